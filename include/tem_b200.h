@@ -1,0 +1,149 @@
+/*
+ * tem_b200.h -- C ABI of the B200-native TEM forward hot path.
+ *
+ * What it computes (PAPER.md, arxiv 2506.11657):
+ *   u(t_j) = exp(-t_j M^-1 K) b,  b = M^-1 f                       (§2.2 eq:expm)
+ * approximated by the shared-pole family (§3.2 eq:ratfam) and evaluated as
+ *   u(t_j) ~ sum_i w_i Re( alpha_ij (K - xi_i M)^-1 f )              (§3.2 eq:rmj)
+ * i.e. one complex-shifted sparse solve (K + s_i M) x_i = f per representative
+ * pole (s_i = -xi_i; w_i = 2 for a conjugate-pair representative, 1 for a real
+ * pole, footnote to eq:rmj) and the tall-skinny product u = 2 Re(S R) (§3.2).
+ *
+ * Discretisation (reading R1): the staggered Yee / finite-
+ * integration grid = lowest-order Nedelec edge elements on a tensor-product
+ * hexahedral grid with lumped masses.  Unknowns are edge line integrals of e;
+ *   K = T^T W T,  (T u)_f = circulation of u around face f,
+ *   W_f = hdual_f / (mu0 A_f),  mu0 = 4 pi 1e-7  (§2.1);
+ *   M_e = (sum_{cells c touching e} sigma_c V_c / 4) / l_e^2;
+ *   f_e = +-I on the transmitter's edges.
+ * Boundary edges (tangential to the outer surface) are fixed to 0 (eq:bc).
+ *
+ * LAYOUTS (all fp64; "device" = CUDA global memory of the current device):
+ *   Nn = (nx+1)(ny+1)(nz+1) nodes, node(i,j,k) = (k*(ny+1)+j)*(nx+1)+i,
+ *   i fastest, z up.  Node (i,j,k) owns edge c (c = 0:x, 1:y, 2:z) from
+ *   node (i,j,k) to node (i,j,k)+e_c.
+ *   - edge vector  (real):    double[3][Nn]            slot = c*Nn + node
+ *   - shift block  (complex): double[3][Nn][S][2]      (re, im) interleaved,
+ *                             slot*S + s; all S shifts of an edge contiguous
+ *   - channel fields (real):  double[K][3][Nn]
+ *   - conductivity:           double[nz][ny][nx]       cell (i,j,k) at [(k*ny+j)*nx+i]
+ *   - complex scalars on the host: double[2*n] (re, im) interleaved
+ *   Slots of non-existent edges (node index == n_c along their own axis) and
+ *   of boundary edges always hold 0 on output.
+ *
+ * OWNERSHIP: every pointer is owned by the caller.  Device buffers are
+ * caller-allocated (PyTorch in the Python binding); the library allocates
+ * only its context (grid spacings, per-shift scalars, reduction scratch, a
+ * cached CUDA graph) and, for tem_forward_host, a device workspace cached in
+ * the context.  `stream` is a cudaStream_t passed as void* (NULL = legacy
+ * default stream).  Calls are asynchronous on `stream` unless stated.
+ *
+ * ERRORS: every call returns 0 on success or a negative TEM_E* code; the
+ * message of the last error on the calling thread is tem_last_error().
+ * Argument errors are detected before any launch; CUDA errors are reported
+ * from the launch that raised them.
+ */
+#ifndef TEM_B200_H
+#define TEM_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TEM_OK 0
+#define TEM_EINVAL -1      /* bad argument (sizes, null pointers, S out of range) */
+#define TEM_ECUDA -2       /* a CUDA runtime call failed */
+#define TEM_ENOMEM -3      /* allocation failed */
+#define TEM_ENOCONV -4     /* tem_cocg_solve: a shift did not converge within maxit */
+#define TEM_EBREAKDOWN -5  /* tem_cocg_solve: COCG breakdown (p^T A p or r^T z == 0) */
+
+#define TEM_MAX_SHIFTS 32  /* S <= 32 representative poles (degree <= 64) */
+
+typedef struct tem_ctx tem_ctx;
+
+/* Library version string, e.g. "tem_b200 0.1 sm_100a". */
+const char* tem_version(void);
+/* Message of the last failed call on this thread ("" if none). */
+const char* tem_last_error(void);
+
+/* Create a context for an nx x ny x nz cell grid with cell widths hx[nx],
+ * hy[ny], hz[nz] (HOST arrays, metres, > 0), on the current CUDA device.
+ * Requires nx, ny, nz >= 2 (at least one interior node plane per axis).
+ * PAPER.md §2.2 (the space V^h): the grid fixes K entirely. */
+int tem_create(int nx, int ny, int nz, const double* hx, const double* hy,
+               const double* hz, tem_ctx** out);
+void tem_destroy(tem_ctx* ctx);
+
+/* Nn = (nx+1)(ny+1)(nz+1), and the number of free (interior) edges N. */
+size_t tem_num_nodes(const tem_ctx* ctx);
+size_t tem_num_unknowns(const tem_ctx* ctx);
+
+/* M_e for every edge from the cell conductivity (§2.2 [M]_ij =
+ * (sigma Phi_j, Phi_i), lumped; reading R1).  sigma: device double[nz][ny][nx]
+ * (> 0); mass: device double[3][Nn] output, 0 on non-free slots. */
+int tem_edge_mass(tem_ctx* ctx, const double* sigma, double* mass, void* stream);
+
+/* Matrix-free multi-shift operator, all shifts in one pass:
+ *   y[:, s] = (K + shifts[s] M) x[:, s],  s = 0..S-1
+ * (§4 "A_i := K - xi_i M", with s = -xi).  x, y: device shift
+ * blocks (complex, [3][Nn][S]); mass from tem_edge_mass; shifts: HOST
+ * complex[S].  Non-free slots of y are written 0.  x's non-free slots MUST
+ * hold 0 (they are the Dirichlet values of eq:bc and enter the stencil of
+ * neighbouring free edges). */
+int tem_apply_shifted(tem_ctx* ctx, const double* mass, int S, const double* shifts,
+                      const double* x, double* y, void* stream);
+
+/* Bytes of device workspace tem_cocg_solve needs for S shifts. */
+size_t tem_cocg_workspace_bytes(const tem_ctx* ctx, int S);
+
+/* Batched multi-shift Jacobi-preconditioned COCG (BASELINE north star (3)):
+ * solves (K + shifts[s] M) x_s = f for every s at once, each shift with its
+ * own COCG scalars and the Jacobi preconditioner D_s = diag(K) + shifts[s] M;
+ * the unconjugated bilinear form a^T b is used for the complex-symmetric
+ * system.  Shift s stops when ||f - A_s x_s||_2 / ||f||_2 <= tol (recursive
+ * residual) or after maxit iterations.
+ *   f:      device edge vector (real, [3][Nn]); only free slots are read
+ *   x:      device shift block output ([3][Nn][S] complex)
+ *   work:   device workspace of >= tem_cocg_workspace_bytes(ctx, S) bytes
+ *   iters, relres (HOST, may be NULL): per-shift iteration count and final
+ *           recursive relative residual.
+ * Returns after the solve has finished (synchronises `stream`).
+ * TEM_ENOCONV if some shift did not reach tol (x still holds its iterate). */
+int tem_cocg_solve(tem_ctx* ctx, const double* mass, const double* f, int S,
+                   const double* shifts, double tol, int maxit, double* x,
+                   void* work, size_t work_bytes, int* iters, double* relres,
+                   void* stream);
+
+/* Statistics of the last tem_cocg_solve on this context. */
+typedef struct {
+  double loop_ms;             /* GPU time (CUDA events) of init + iteration loop */
+  long long kernel_launches;  /* kernels launched by the solve */
+  long long shift_iterations; /* sum over shifts of COCG iterations */
+  int iterations;             /* max over shifts */
+  int grid, block;            /* launch configuration of the sweep kernels */
+} tem_solve_stats;
+int tem_last_solve_stats(const tem_ctx* ctx, tem_solve_stats* out);
+
+/* Channel synthesis, the tall-skinny product of §3.2 (eq:rmj):
+ *   u[k][slot] = sum_s w_s Re( residues[k*S + s] * x[slot][s] ),
+ *   w_s = 2 if is_pair[s] else 1,   k = 0..K-1
+ * residues: HOST complex[K][S]; is_pair: HOST int[S]; x: device shift block;
+ * u: device double[K][3][Nn] (non-free slots written 0). */
+int tem_synthesize(tem_ctx* ctx, int S, int K, const double* residues, const int* is_pair,
+                   const double* x, double* u, void* stream);
+
+/* End-to-end forward with HOST buffers: uploads sigma and f, computes the
+ * mass, solves all shifted systems, synthesises all K channels and downloads
+ * u (HOST double[K][3][Nn]).  Device memory comes from a workspace cached in
+ * the context.  Synchronous.  Same error codes as tem_cocg_solve. */
+int tem_forward_host(tem_ctx* ctx, const double* sigma, const double* f, int S,
+                     const double* shifts, int K, const double* residues,
+                     const int* is_pair, double tol, int maxit, double* u,
+                     int* iters, double* relres);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TEM_B200_H */

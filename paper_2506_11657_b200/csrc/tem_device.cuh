@@ -1,0 +1,102 @@
+// tem_device.cuh -- device-side building blocks of the B200 TEM hot path.
+//
+// Yee / finite-integration curl-curl on the node-owned edge layout of
+// include/tem_b200.h (reading R1):
+//   (K u)_a(m) = W_d(m) C_d(m) - W_d(m-e_b) C_d(m-e_b) - W_b(m) C_b(m) + W_b(m-e_d) C_b(m-e_d)
+// for the edge along axis a at node m, (a, b, d) a cyclic permutation of
+// (x, y, z), where C_d(m') is the circulation around the face normal to d
+// with lower corner m' (right-hand rule about +d):
+//   C_d(m') = u_a(m') + u_b(m'+e_a) - u_a(m'+e_b) - u_b(m')
+//   C_b(m') = u_d(m') + u_a(m'+e_d) - u_d(m'+e_a) - u_a(m')
+// and W_d(m') = hdual_d[m'_d] / (mu0 h_a[m'_a] h_b[m'_b]).  This is
+// K = T^T W T (§2.2 [K]_ij = (mu^-1 curl Phi_j, curl Phi_i)) written
+// as a 13-point gather; nothing is assembled.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tem {
+
+constexpr double kMu0 = 4e-7 * 3.14159265358979323846;  // PAPER.md §2.1
+
+struct Grid {
+  int n[3];               // cells per axis
+  long long st[3];        // node strides: 1, nx+1, (nx+1)(ny+1)
+  long long Nn;           // nodes
+  const double* ih[3];    // 1 / h_a[i], i < n_a                     (device)
+  const double* hdm[3];   // hdual_a[i] / mu0, i = 0..n_a             (device)
+};
+
+// ---------------------------------------------------------------- complex
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cscale(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a + b*c
+__device__ __forceinline__ double2 cfma(double2 b, double2 c, double2 a) {
+  return make_double2(fma(b.x, c.x, fma(-b.y, c.y, a.x)), fma(b.x, c.y, fma(b.y, c.x, a.y)));
+}
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
+  const double inv = 1.0 / fma(b.x, b.x, b.y * b.y);
+  return make_double2(fma(a.x, b.x, a.y * b.y) * inv, fma(a.y, b.x, -a.x * b.y) * inv);
+}
+__device__ __forceinline__ double2 czero() { return make_double2(0.0, 0.0); }
+
+// Face weights of the four faces around edge (A, pos): W_d(m), W_d(m-e_b), W_b(m), W_b(m-e_d).
+struct EdgeWeights {
+  double wd0, wd1, wb0, wb1;
+  __device__ __forceinline__ double diag() const { return wd0 + wd1 + wb0 + wb1; }
+};
+
+template <int A>
+__device__ __forceinline__ EdgeWeights edge_weights(const Grid& g, const int pos[3]) {
+  constexpr int B = (A + 1) % 3, D = (A + 2) % 3;
+  const double iha = __ldg(g.ih[A] + pos[A]);
+  const double hdD = __ldg(g.hdm[D] + pos[D]);
+  const double hdB = __ldg(g.hdm[B] + pos[B]);
+  EdgeWeights w;
+  w.wd0 = hdD * iha * __ldg(g.ih[B] + pos[B]);
+  w.wd1 = hdD * iha * __ldg(g.ih[B] + pos[B] - 1);
+  w.wb0 = hdB * iha * __ldg(g.ih[D] + pos[D]);
+  w.wb1 = hdB * iha * __ldg(g.ih[D] + pos[D] - 1);
+  return w;
+}
+
+// (K v)_A at node n for shift lane s of a complex shift block v[3][Nn][S].
+// Only called for free edges (all 12 neighbours exist and non-free ones hold 0).
+template <int A>
+__device__ __forceinline__ double2 curlcurl(const Grid& g, const double2* __restrict__ v,
+                                            long long n, int s, int S, const EdgeWeights& w,
+                                            double2 a0) {
+  constexpr int B = (A + 1) % 3, D = (A + 2) % 3;
+  const long long sA = g.st[A], sB = g.st[B], sD = g.st[D];
+  const double2* va = v + (long long)A * g.Nn * S + s;
+  const double2* vb = v + (long long)B * g.Nn * S + s;
+  const double2* vd = v + (long long)D * g.Nn * S + s;
+#define TEM_LD(arr, node) __ldg((arr) + (node) * S)
+  // face normal to D at m and at m - e_B
+  const double2 cD0 = csub(cadd(a0, TEM_LD(vb, n + sA)), cadd(TEM_LD(va, n + sB), TEM_LD(vb, n)));
+  const double2 cD1 = csub(cadd(TEM_LD(va, n - sB), TEM_LD(vb, n - sB + sA)),
+                           cadd(a0, TEM_LD(vb, n - sB)));
+  // face normal to B at m and at m - e_D
+  const double2 cB0 = csub(cadd(TEM_LD(vd, n), TEM_LD(va, n + sD)), cadd(TEM_LD(vd, n + sA), a0));
+  const double2 cB1 = csub(cadd(TEM_LD(vd, n - sD), a0),
+                           cadd(TEM_LD(vd, n - sD + sA), TEM_LD(va, n - sD)));
+#undef TEM_LD
+  double2 r;
+  r.x = w.wd0 * cD0.x - w.wd1 * cD1.x - w.wb0 * cB0.x + w.wb1 * cB1.x;
+  r.y = w.wd0 * cD0.y - w.wd1 * cD1.y - w.wb0 * cB0.y + w.wb1 * cB1.y;
+  return r;
+}
+
+__device__ __forceinline__ void node_pos(const Grid& g, long long n, int pos[3]) {
+  const long long nx1 = g.n[0] + 1, ny1 = g.n[1] + 1;
+  const long long q = n / nx1;
+  pos[0] = (int)(n - q * nx1);
+  pos[1] = (int)(q % ny1);
+  pos[2] = (int)(q / ny1);
+}
+
+}  // namespace tem

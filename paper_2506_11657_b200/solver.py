@@ -1,0 +1,239 @@
+"""Python face of the C ABI (include/tem_b200.h) -- marshalling only.
+
+Every numerical step runs in libtem_b200.so's sm_100a kernels; this module
+only moves pointers, sizes and small host arrays across the boundary.
+PyTorch provides device memory and streams.
+
+    fw = TemForward(hx, hy, hz)                 # grid (§2.2)
+    mass = fw.edge_mass(sigma)                  # M, lumped          (§2.2)
+    x, iters, relres = fw.cocg(mass, f, shifts) # (K + s_i M) x_i = f (§3.2, eq:rmj)
+    u = fw.synthesize(x, residues, is_pair)     # u(t_j) = 2 Re(S R)  (§3.2)
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+
+import numpy as np
+import torch
+
+from . import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _iptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int))
+
+
+def _cplx(z) -> np.ndarray:
+    """complex array -> contiguous interleaved (re, im) float64."""
+    z = np.ascontiguousarray(np.asarray(z, dtype=np.complex128))
+    return np.ascontiguousarray(z.view(np.float64).reshape(-1))
+
+
+def _stream_ptr(stream) -> ctypes.c_void_p:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _need_cuda(t: torch.Tensor, dtype, name: str):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU path)")
+    if t.dtype != dtype or not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous {dtype}")
+
+
+class RationalTable:
+    """Shared poles and residue table (§3.2 eq:ratfam) in the
+    physical variable: shifts s_i = -xi_i (1/s), residues (n_shift, K),
+    is_pair (w_i = 2 for a conjugate pair, eq:rmj)."""
+
+    def __init__(self, shifts, residues, is_pair, times, uniform_error=None):
+        self.shifts = np.asarray(shifts, dtype=np.complex128)
+        self.residues = np.asarray(residues, dtype=np.complex128)
+        self.is_pair = np.asarray(is_pair, dtype=bool)
+        self.times = np.asarray(times, dtype=np.float64)
+        self.uniform_error = uniform_error
+
+    @property
+    def n_shift(self) -> int:
+        return self.shifts.size
+
+    @classmethod
+    def load(cls, name_or_path: str) -> "RationalTable":
+        """Read data/rational/<name>.json (inputs computed once on the host
+        by scripts/make_rational_tables.py)."""
+        path = name_or_path
+        if not os.path.exists(path):
+            path = os.path.join(ROOT, "data", "rational", f"{name_or_path}.json")
+        with open(path) as fh:
+            t = json.load(fh)
+
+        def c(lst):
+            return np.array([complex(a, b) for a, b in lst])
+        return cls(c(t["shifts"]), np.stack([c(r) for r in t["residues"]]), t["is_pair"],
+                   t["times"], t.get("uniform_error"))
+
+
+class TemForward:
+    """One tensor grid on one GPU.  All device buffers are torch tensors."""
+
+    def __init__(self, hx, hy, hz, device=None):
+        self.lib = _lib.load()
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None \
+            else torch.device(device)
+        if self.device.type != "cuda":
+            raise ValueError("TemForward runs on CUDA only")
+        self.hx = np.ascontiguousarray(hx, dtype=np.float64)
+        self.hy = np.ascontiguousarray(hy, dtype=np.float64)
+        self.hz = np.ascontiguousarray(hz, dtype=np.float64)
+        self.shape = (self.hx.size, self.hy.size, self.hz.size)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.tem_create(*self.shape, _dptr(self.hx), _dptr(self.hy),
+                                           _dptr(self.hz), ctypes.byref(h)))
+        self._h = h
+        self.Nn = int(self.lib.tem_num_nodes(h))
+        self.n_unknowns = int(self.lib.tem_num_unknowns(h))
+        self._work = {}
+
+    def close(self):
+        if self._h:
+            self.lib.tem_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ layout
+    @property
+    def n_slots(self) -> int:
+        return 3 * self.Nn
+
+    def slot(self, c, i, j, k):
+        """Slot index of edge (c, i, j, k) in an edge vector ([3][Nn])."""
+        nx, ny, _ = self.shape
+        return np.asarray(c) * self.Nn + (np.asarray(k) * (ny + 1) + np.asarray(j)) * (nx + 1) \
+            + np.asarray(i)
+
+    def source_vector(self, source_edges, current: float = 1.0) -> np.ndarray:
+        """Host edge vector f: +-I on the transmitter's edges (layout only)."""
+        f = np.zeros(self.n_slots)
+        for (c, i, j, k, s) in source_edges:
+            f[self.slot(c, i, j, k)] += s * current
+        return f
+
+    def sigma_layout(self, sigma: np.ndarray) -> np.ndarray:
+        nx, ny, nz = self.shape
+        sigma = np.ascontiguousarray(sigma, dtype=np.float64)
+        if sigma.shape != (nz, ny, nx):
+            raise ValueError(f"sigma must have shape (nz, ny, nx) = {(nz, ny, nx)}")
+        return sigma
+
+    # ------------------------------------------------------------ calls
+    def edge_mass(self, sigma: torch.Tensor, stream=None) -> torch.Tensor:
+        _need_cuda(sigma, torch.float64, "sigma")
+        if sigma.numel() != self.shape[0] * self.shape[1] * self.shape[2]:
+            raise ValueError("sigma size mismatch")
+        mass = torch.empty(self.n_slots, dtype=torch.float64, device=self.device)
+        _lib.check(self.lib.tem_edge_mass(self._h, ctypes.c_void_p(sigma.data_ptr()),
+                                          ctypes.c_void_p(mass.data_ptr()), _stream_ptr(stream)))
+        return mass
+
+    def apply(self, mass: torch.Tensor, shifts, x: torch.Tensor, stream=None) -> torch.Tensor:
+        """y[:, s] = (K + s M) x[:, s]; x is complex128 (n_slots, S)."""
+        sh = _cplx(shifts)
+        S = sh.size // 2
+        _need_cuda(x, torch.complex128, "x")
+        if x.shape != (self.n_slots, S):
+            raise ValueError(f"x must be (n_slots, S) = {(self.n_slots, S)}")
+        y = torch.empty_like(x)
+        _lib.check(self.lib.tem_apply_shifted(self._h, ctypes.c_void_p(mass.data_ptr()), S,
+                                              _dptr(sh), ctypes.c_void_p(x.data_ptr()),
+                                              ctypes.c_void_p(y.data_ptr()), _stream_ptr(stream)))
+        return y
+
+    def workspace(self, S: int) -> torch.Tensor:
+        if S not in self._work:
+            nbytes = int(self.lib.tem_cocg_workspace_bytes(self._h, S))
+            self._work[S] = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        return self._work[S]
+
+    def cocg(self, mass: torch.Tensor, f: torch.Tensor, shifts, tol: float = 1e-10,
+             maxit: int = 100000, x: torch.Tensor | None = None, stream=None,
+             raise_on_noconv: bool = True):
+        """Batched multi-shift Jacobi-COCG.  Returns (x, iters, relres)."""
+        _need_cuda(mass, torch.float64, "mass")
+        _need_cuda(f, torch.float64, "f")
+        sh = _cplx(shifts)
+        S = sh.size // 2
+        if x is None:
+            x = torch.empty((self.n_slots, S), dtype=torch.complex128, device=self.device)
+        work = self.workspace(S)
+        iters = np.zeros(S, dtype=np.int32)
+        relres = np.zeros(S, dtype=np.float64)
+        rc = self.lib.tem_cocg_solve(self._h, ctypes.c_void_p(mass.data_ptr()),
+                                     ctypes.c_void_p(f.data_ptr()), S, _dptr(sh), float(tol),
+                                     int(maxit), ctypes.c_void_p(x.data_ptr()),
+                                     ctypes.c_void_p(work.data_ptr()), work.numel(),
+                                     _iptr(iters), _dptr(relres), _stream_ptr(stream))
+        if rc != 0 and (raise_on_noconv or rc != _lib.TEM_ENOCONV):
+            _lib.check(rc)
+        return x, iters, relres
+
+    def stats(self) -> dict:
+        st = _lib.SolveStats()
+        _lib.check(self.lib.tem_last_solve_stats(self._h, ctypes.byref(st)))
+        return {k: getattr(st, k) for k, _ in _lib.SolveStats._fields_}
+
+    def synthesize(self, x: torch.Tensor, residues, is_pair, stream=None) -> torch.Tensor:
+        """u[k] = sum_s w_s Re(residues[s, k] x[:, s]); residues (S, K)."""
+        res = np.asarray(residues, dtype=np.complex128)
+        S, K = res.shape
+        _need_cuda(x, torch.complex128, "x")
+        if x.shape != (self.n_slots, S):
+            raise ValueError("x shape mismatch")
+        r = _cplx(res.T.copy())           # ABI wants [K][S]
+        ip = np.ascontiguousarray(np.asarray(is_pair, dtype=np.int32))
+        u = torch.empty((K, self.n_slots), dtype=torch.float64, device=self.device)
+        _lib.check(self.lib.tem_synthesize(self._h, S, K, _dptr(r), _iptr(ip),
+                                           ctypes.c_void_p(x.data_ptr()),
+                                           ctypes.c_void_p(u.data_ptr()), _stream_ptr(stream)))
+        return u
+
+    def forward_host(self, sigma: np.ndarray, f: np.ndarray, table: RationalTable,
+                     tol: float = 1e-10, maxit: int = 100000, out: np.ndarray | None = None):
+        """End-to-end with host buffers (tem_forward_host).  Returns
+        (u (K, n_slots) host array, iters, relres)."""
+        sig = self.sigma_layout(sigma)
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        S, K = table.residues.shape
+        sh = _cplx(table.shifts)
+        r = _cplx(table.residues.T.copy())
+        ip = np.ascontiguousarray(table.is_pair.astype(np.int32))
+        u = np.empty((K, self.n_slots)) if out is None else out
+        iters = np.zeros(S, dtype=np.int32)
+        relres = np.zeros(S)
+        with torch.cuda.device(self.device):
+            rc = self.lib.tem_forward_host(self._h, _dptr(sig), _dptr(f), S, _dptr(sh), K,
+                                           _dptr(r), _iptr(ip), float(tol), int(maxit),
+                                           _dptr(u), _iptr(iters), _dptr(relres))
+        _lib.check(rc)
+        return u, iters, relres
+
+    def forward(self, sigma: torch.Tensor, f: torch.Tensor, table: RationalTable,
+                tol: float = 1e-10, maxit: int = 100000, stream=None):
+        """Device-resident forward: mass, COCG, synthesis.  Returns (u, x, iters, relres)."""
+        mass = self.edge_mass(sigma, stream)
+        x, iters, relres = self.cocg(mass, f, table.shifts, tol, maxit, stream=stream)
+        u = self.synthesize(x, table.residues, table.is_pair, stream)
+        return u, x, iters, relres

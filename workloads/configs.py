@@ -205,8 +205,10 @@ def make_custom(nx: int, ny: int, nz: int, h: float = 50.0, n_air: int = 2,
     sigma = _air(sigma, n_air)
     k_s = nz - n_air
     ci, cj = nx // 2, ny // 2
-    src = loop_source_edges(max(ci - loop_half, 1), min(ci + loop_half, nx - 1),
-                            max(cj - loop_half, 1), min(cj + loop_half, ny - 1), k_s)
+    i0, i1 = max(ci - loop_half, 1), min(ci + loop_half, nx - 1)
+    j0, j1 = max(cj - loop_half, 1), min(cj + loop_half, ny - 1)
+    ok = i1 > i0 and j1 > j0 and 1 <= k_s <= nz - 1
+    src = loop_source_edges(i0, i1, j0, j1, k_s) if ok else []
     if times is None:
         times = time_channels(1e-5, 1e-2, 31)
     return Workload(f"custom{nx}x{ny}x{nz}", g, sigma, src, np.asarray(times), n_poles, n_air)
