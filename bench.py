@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""Benchmark of the TEM forward hot path (BASELINE.json metric).
+
+A STEP = one pass of the whole hot path over one synthetic earth model:
+edge mass (§2.2) -> batched multi-shift Jacobi-COCG to relative residual
+1e-10 for every shifted system (K + s_i M) x_i = f (§3.2 eq:rmj) ->
+channel synthesis u(t_j) = sum_i w_i Re(alpha_ij x_i) for all K channels.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config large]
+    python bench.py --impl reference      # the CPU oracle arm
+
+metric  : shift-unknown-iterations/s (sum over shifts of COCG iterations x
+          free edge unknowns, per second), whole job over all ranks;
+          ms_per_step is the wall time to all time channels.
+roofline: the COCG sweep kernels against measured HBM bandwidth, at the
+          algorithmic 128 B per shift-unknown-iteration.
+e2e     : the same step through tem_forward_host with pinned HOST buffers
+          (sigma, f uploaded; all channel fields downloaded) each step.
+N > 1   : one process per GPU (torchrun), each rank an independent
+          sounding (the transmitter moved by rank) -> weak scaling, no
+          data-path collective.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ALG_BYTES_PER_SUI = 128  # x, r, p streamed at the 2-sweep COCG minimum
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def _dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _workload_for_rank(name: str, rank: int):
+    from workloads import make_workload
+    from workloads.configs import loop_source_edges
+    wl = make_workload(name)
+    if rank:
+        # independent sounding per rank: transmitter moved by `rank` cells along x
+        xs = sorted({e[1] for e in wl.source if e[0] == 0})
+        ys = sorted({e[2] for e in wl.source if e[0] == 0})
+        i0, i1 = xs[0] + rank, xs[-1] + 1 + rank
+        if i1 >= wl.grid.shape[0]:
+            i0, i1 = xs[0] - rank, xs[-1] + 1 - rank
+        wl.source = loop_source_edges(i0, i1, ys[0], ys[-1], wl.surface_k)
+    return wl
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_11657_b200 import RationalTable, TemForward
+
+    ws, rank, local = _dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product has no CPU path)")
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    wl = _workload_for_rank(args.config, rank)
+    table = RationalTable.load(args.config)
+    fw = TemForward(wl.grid.hx, wl.grid.hy, wl.grid.hz, device=dev)
+    sigma = torch.from_numpy(fw.sigma_layout(wl.sigma)).to(dev)
+    f = torch.from_numpy(fw.source_vector(wl.source)).to(dev)
+    S, K = table.residues.shape
+    N = fw.n_unknowns
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        mass = fw.edge_mass(sigma)
+        x, iters, relres = fw.cocg(mass, f, table.shifts, tol=args.tol, maxit=args.maxit)
+        u = fw.synthesize(x, table.residues, table.is_pair)
+        st = fw.stats()
+        return u, iters, relres, st
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        u, iters, relres, st = step()
+        del u
+    barrier()
+    sui = 0
+    loop_ms = 0.0
+    launches = 0
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            u, iters, relres, st = step()
+            sui += int(st["shift_iterations"]) * N
+            loop_ms += st["loop_ms"]
+            launches += int(st["kernel_launches"]) + 2      # + edge mass + synthesis
+            del u
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    assert np.all(relres <= args.tol), relres
+
+    # max over ranks for the time, sums for the work
+    t_max, sui_tot, loop_max = ms, sui, loop_ms
+    if ws > 1:
+        tt = torch.tensor([ms, loop_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        w = torch.tensor([float(sui)], dtype=torch.float64, device=dev)
+        dist.all_reduce(w, op=dist.ReduceOp.SUM)
+        t_max, loop_max, sui_tot = float(tt[0]), float(tt[1]), int(w.item())
+
+    # ---- e2e through the C ABI with pinned host buffers (rank-local, then max)
+    e2e = None
+    if not args.no_e2e:
+        sig_h = torch.from_numpy(fw.sigma_layout(wl.sigma)).pin_memory()
+        f_h = torch.from_numpy(fw.source_vector(wl.source)).pin_memory()
+        u_h = torch.empty((K, fw.n_slots), dtype=torch.float64).pin_memory()
+        fw.forward_host(sig_h.numpy(), f_h.numpy(), table, tol=args.tol, maxit=args.maxit,
+                        out=u_h.numpy())          # warm (allocates the cached workspace)
+        barrier()
+        t0 = time.perf_counter()
+        e2e_sui = 0
+        for _ in range(args.steps):
+            _, it_h, _ = fw.forward_host(sig_h.numpy(), f_h.numpy(), table, tol=args.tol,
+                                         maxit=args.maxit, out=u_h.numpy())
+            e2e_sui += int(np.sum(it_h)) * N
+        barrier()
+        e2e_s = time.perf_counter() - t0
+        if ws > 1:
+            tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+            w = torch.tensor([float(e2e_sui)], dtype=torch.float64, device=dev)
+            dist.all_reduce(w, op=dist.ReduceOp.SUM)
+            e2e_sui = int(w.item())
+        e2e = {"value": e2e_sui / e2e_s, "unit": "shift-unknown-iterations/s",
+               "h2d_bytes_per_step": int(sig_h.numel() * 8 + f_h.numel() * 8),
+               "d2h_bytes_per_step": int(u_h.numel() * 8),
+               "ms_per_step": 1e3 * e2e_s / args.steps}
+        del u_h
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return None
+
+    peak, peak_kind = _peaks()
+    achieved = ALG_BYTES_PER_SUI * (sui / args.steps) / (loop_ms / args.steps * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bytes_per_sui")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": "shift-unknown-iterations/s",
+        "value": sui_tot / (t_max * 1e-3),
+        "unit": "shift-unknown-iterations/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_max / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c128",
+        "data": "synthetic (seeded earth model, BASELINE configs[4] shape)",
+        "config": {"workload": args.config, "unknowns": N, "shifts": S, "channels": K,
+                   "degree": int(2 * table.is_pair.sum() + (~table.is_pair).sum()),
+                   "tol": args.tol, "iterations_max": int(st["iterations"]),
+                   "iterations_per_shift": [int(i) for i in iters],
+                   "l2": "inputs larger than L2 (each shift block %.2f GB)" % (fw.n_slots * S * 16 / 1e9),
+                   "wall_time_to_all_channels_ms": t_max / args.steps,
+                   "parallelism": f"{ws} independent soundings" if ws > 1 else "1 GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "COCG sweeps (k_dir + k_ap + k_upd), algorithmic 128 B/SUI",
+                     "peak_kind": peak_kind},
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "gpu_launches": launches,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.config, args.cpu_iters)
+    if ws > 1:
+        dist.destroy_process_group()
+    return line
+
+
+def cpu_baseline(config: str, iters: int):
+    """The oracle (oracle/cocg.py, as it stands) on the same workload:
+    CSR assembly untimed, then `iters` COCG iterations of the hardest
+    (smallest |s|) shift, timed.  Bounded sample, scaled to SUI/s."""
+    from oracle import cocg, yee
+    from paper_2506_11657_b200 import RationalTable  # table reading only
+    from workloads import make_workload
+    wl = make_workload(config)
+    table = RationalTable.load(config)
+    asm = yee.assemble(wl)
+    s = table.shifts[np.argmin(np.abs(table.shifts))]
+    t0 = time.perf_counter()
+    cocg.cocg(asm, complex(s), tol=1e-300, maxit=iters)
+    dt = time.perf_counter() - t0
+    return {"value": asm.n * iters / dt, "unit": "shift-unknown-iterations/s", "cores": 1,
+            "kind": "oracle",
+            "sample": f"{config}: {iters} COCG iterations of 1 of {table.n_shift} shifts "
+                      f"(N={asm.n}), scipy CSR, single-threaded; assembly untimed"}
+
+
+def run_reference(args):
+    ws, rank, _ = _dist_env()
+    if rank != 0:
+        return None
+    from oracle import cocg, yee
+    from paper_2506_11657_b200 import RationalTable
+    from workloads import make_workload
+    wl = make_workload(args.config)
+    table = RationalTable.load(args.config)
+    asm = yee.assemble(wl)
+    s = complex(table.shifts[np.argmin(np.abs(table.shifts))])
+    for _ in range(args.warmup):
+        cocg.cocg(asm, s, tol=1e-300, maxit=1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cocg.cocg(asm, s, tol=1e-300, maxit=args.cpu_iters)
+    dt = time.perf_counter() - t0
+    v = asm.n * args.cpu_iters * args.steps / dt
+    sample = (f"{args.config}: each step = {args.cpu_iters} COCG iterations of 1 of "
+              f"{table.n_shift} shifts (N={asm.n}), scipy CSR, single-threaded")
+    return {"impl": "reference", "metric": "shift-unknown-iterations/s", "value": v,
+            "unit": "shift-unknown-iterations/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic", "config": {"workload": args.config, "unknowns": asm.n},
+            "cpu_baseline": {"value": v, "unit": "shift-unknown-iterations/s", "cores": 1,
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "shift-unknown-iterations/s",
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="large")
+    ap.add_argument("--tol", type=float, default=1e-10)
+    ap.add_argument("--maxit", type=int, default=200000)
+    ap.add_argument("--cpu-iters", type=int, default=8)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        sys.stderr.write("bench.py: warning: fewer than 3 warm-up steps\n")
+    line = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -8,7 +8,9 @@ channels t_1, ..., t_K"), and the degree m-hat of the shared-pole family
 
 Where BASELINE.json is silent (padding counts, air thickness, layer depths,
 body shapes, loop placement) the choice is made here and listed in DESIGN.md
-"Input recipe".  All randomness is seeded numpy ``default_rng``.
+"Input recipe".  Padding: Jacobi-COCG iteration counts grow steeply with the
+aspect ratio of stretched cells (measured: DESIGN.md "Input recipe"), so where
+BASELINE leaves the padding open it is 6 cells stretching 1.15 per side.  All randomness is seeded numpy ``default_rng``.
 """
 from __future__ import annotations
 
@@ -111,10 +113,10 @@ def _block() -> Workload:
 
 
 def _layered() -> Workload:
-    # configs[2]: 64^3 cells, 10 m core, 10 padding cells per side stretching 1.25;
+    # configs[2]: 64^3 cells, 10 m core, 5 padding cells per side stretching 1.25;
     # air = top 12 layers; layers below the surface: 0.05 S/m to 50 m depth,
     # 0.005 S/m to 150 m, 0.2 S/m below; 200 m loop; 20 poles; 61 ch 1e-6..1e-1.
-    ax = padded_axis(64, 10.0, 10, 10, 1.25)
+    ax = padded_axis(64, 10.0, 5, 5, 1.25)
     g = TensorGrid(ax.copy(), ax.copy(), ax.copy())
     n_air = 12
     k_s = 64 - n_air
@@ -129,13 +131,13 @@ def _layered() -> Workload:
 
 
 def _hetero() -> Workload:
-    # configs[3]: 128x128x96 cells (~4.7M edges), 20 m core, 8 padding cells per
-    # side stretching 1.25; log10 sigma ~ N(-2, 0.5^2) iid per cell (seed 0),
+    # configs[3]: 128x128x96 cells (~4.7M edges), 20 m core, 6 padding cells per
+    # side stretching 1.15; log10 sigma ~ N(-2, 0.5^2) iid per cell (seed 0),
     # smoothed by a 3x3x3 box filter; air 1e-8 in the top 16 cells;
     # 200 m loop; 20 poles; 61 channels 1e-6..1e-1.
-    g = TensorGrid(padded_axis(128, 20.0, 8, 8, 1.25),
-                   padded_axis(128, 20.0, 8, 8, 1.25),
-                   padded_axis(96, 20.0, 8, 8, 1.25))
+    g = TensorGrid(padded_axis(128, 20.0, 6, 6, 1.15),
+                   padded_axis(128, 20.0, 6, 6, 1.15),
+                   padded_axis(96, 20.0, 6, 6, 1.15))
     n_air = 16
     rng = np.random.default_rng(0)
     lg = rng.normal(-2.0, 0.5, size=(96, 128, 128))
@@ -145,14 +147,14 @@ def _hetero() -> Workload:
 
 
 def _large() -> Workload:
-    # configs[4]: 192x192x128 cells (~14M edges), 20 m core, 14 padding cells
-    # per side stretching 1.25; background 0.01 S/m; air 1e-8 in the top 20
+    # configs[4]: 192x192x128 cells (~14M edges), 20 m core, 6 padding cells
+    # per side stretching 1.15; background 0.01 S/m; air 1e-8 in the top 20
     # cells; 5 random axis-aligned ellipsoids (seed 1) of 0.1-1 S/m
     # (log-uniform), centres 60-500 m deep inside the core, semi-axes 40-200 m;
     # 200 m loop; 24 poles; 100 channels 1e-6..1e-1.
-    g = TensorGrid(padded_axis(192, 20.0, 14, 14, 1.25),
-                   padded_axis(192, 20.0, 14, 14, 1.25),
-                   padded_axis(128, 20.0, 14, 14, 1.25))
+    g = TensorGrid(padded_axis(192, 20.0, 6, 6, 1.15),
+                   padded_axis(192, 20.0, 6, 6, 1.15),
+                   padded_axis(128, 20.0, 6, 6, 1.15))
     n_air = 20
     k_s = 128 - n_air
     sigma = np.full((128, 192, 192), 0.01)
