@@ -23,8 +23,10 @@
  *   i fastest, z up.  Node (i,j,k) owns edge c (c = 0:x, 1:y, 2:z) from
  *   node (i,j,k) to node (i,j,k)+e_c.
  *   - edge vector  (real):    double[3][Nn]            slot = c*Nn + node
- *   - shift block  (complex): double[3][Nn][S][2]      (re, im) interleaved,
- *                             slot*S + s; all S shifts of an edge contiguous
+ *   - shift block  (complex): double[S][3][Nn][2]      (re, im) interleaved,
+ *                             s*3*Nn + slot (shift-major: one edge vector per
+ *                             shift, so a CTA sweeping one shift streams it
+ *                             contiguously and converged shifts cost nothing)
  *   - channel fields (real):  double[K][3][Nn]
  *   - conductivity:           double[nz][ny][nx]       cell (i,j,k) at [(k*ny+j)*nx+i]
  *   - complex scalars on the host: double[2*n] (re, im) interleaved
@@ -88,7 +90,7 @@ int tem_edge_mass(tem_ctx* ctx, const double* sigma, double* mass, void* stream)
 /* Matrix-free multi-shift operator, all shifts in one pass:
  *   y[:, s] = (K + shifts[s] M) x[:, s],  s = 0..S-1
  * (§4 "A_i := K - xi_i M", with s = -xi).  x, y: device shift
- * blocks (complex, [3][Nn][S]); mass from tem_edge_mass; shifts: HOST
+ * blocks (complex, [S][3][Nn]); mass from tem_edge_mass; shifts: HOST
  * complex[S].  Non-free slots of y are written 0.  x's non-free slots MUST
  * hold 0 (they are the Dirichlet values of eq:bc and enter the stencil of
  * neighbouring free edges). */
@@ -105,7 +107,7 @@ size_t tem_cocg_workspace_bytes(const tem_ctx* ctx, int S);
  * system.  Shift s stops when ||f - A_s x_s||_2 / ||f||_2 <= tol (recursive
  * residual) or after maxit iterations.
  *   f:      device edge vector (real, [3][Nn]); only free slots are read
- *   x:      device shift block output ([3][Nn][S] complex)
+ *   x:      device shift block output ([S][3][Nn] complex)
  *   work:   device workspace of >= tem_cocg_workspace_bytes(ctx, S) bytes
  *   iters, relres (HOST, may be NULL): per-shift iteration count and final
  *           recursive relative residual.
@@ -127,7 +129,7 @@ typedef struct {
 int tem_last_solve_stats(const tem_ctx* ctx, tem_solve_stats* out);
 
 /* Channel synthesis, the tall-skinny product of §3.2 (eq:rmj):
- *   u[k][slot] = sum_s w_s Re( residues[k*S + s] * x[slot][s] ),
+ *   u[k][slot] = sum_s w_s Re( residues[k*S + s] * x[s][slot] ),
  *   w_s = 2 if is_pair[s] else 1,   k = 0..K-1
  * residues: HOST complex[K][S]; is_pair: HOST int[S]; x: device shift block;
  * u: device double[K][3][Nn] (non-free slots written 0). */

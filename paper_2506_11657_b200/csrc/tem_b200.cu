@@ -34,6 +34,7 @@
 
 #include "../../include/tem_b200.h"
 #include "tem_device.cuh"
+#include "tem_sweep.cuh"
 
 using tem::Grid;
 
@@ -54,85 +55,6 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 constexpr int kChunk = 16;          // iterations per captured graph
-constexpr int kMaxGridMult = 16;    // partials sized for numSMs * kMaxGridMult CTAs
-constexpr int kTargetThreads = 256; // CTA size target (tile = floor(256/S) nodes x S shifts)
-
-struct ShiftState {
-  double2 s;        // shift
-  double2 rho;      // r^T z
-  double2 alpha;
-  double2 beta;
-  double fnorm;     // ||f||_2
-  double relres;    // ||r||_2 / ||f||_2
-  int active;
-  int iters;
-  int status;       // 0 running, 1 converged, 2 breakdown
-  int pad;
-};
-
-struct Control {
-  double tol;
-  int n_active;
-  unsigned int ticket[4];
-};
-
-struct SolveArgs {
-  Grid g;
-  int S;
-  int tile_nodes;
-  long long ntiles;
-  const double* mass;   // [3][Nn]
-  const double* f;      // [3][Nn]
-  double2* x;           // [3][Nn][S]
-  double2* r;
-  double2* p;
-  ShiftState* st;       // [S]
-  Control* ctl;
-  double2* part_c;      // [grid][S]
-  double* part_r;       // [grid][S]
-};
-
-// ------------------------------------------------------------------ helpers
-
-// Per-shift block reduction of one value per thread (thread = node_local*S + s).
-// Threads s < S end up with the block sum for shift s (deterministic order).
-template <typename T>
-__device__ __forceinline__ T block_sum_per_shift(T v, T* buf, int S, int tile_nodes) {
-  buf[threadIdx.x] = v;
-  __syncthreads();
-  T acc{};
-  if ((int)threadIdx.x < S) {
-    for (int nl = 0; nl < tile_nodes; ++nl) acc += buf[nl * S + threadIdx.x];
-  }
-  __syncthreads();
-  return acc;
-}
-__device__ __forceinline__ double2& operator+=(double2& a, const double2& b) {
-  a.x += b.x;
-  a.y += b.y;
-  return a;
-}
-
-// The last CTA of a launch (atomic ticket) reduces the per-CTA partials per
-// shift: warp w handles shifts w, w + nwarps, ...; lanes stride over CTAs;
-// fixed shuffle tree.  Returns true in the finalising CTA.
-__device__ bool last_block(unsigned int* ticket) {
-  __shared__ bool am_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned int t = atomicAdd(ticket, 1u);
-    am_last = (t == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (am_last) __threadfence();
-  return am_last;
-}
-
-__device__ __forceinline__ double warp_sum(double v) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  return v;
-}
 
 // ------------------------------------------------------------------ kernels
 
@@ -166,105 +88,64 @@ __global__ void k_edge_mass(Grid g, const double* __restrict__ sigma, double* __
   }
 }
 
-struct ShiftList {
-  double2 s[TEM_MAX_SHIFTS];
-};
-
-template <int A>
-__device__ __forceinline__ void apply_one(const Grid& g, const double* __restrict__ mass,
-                                          const double2* __restrict__ x, double2* __restrict__ y,
-                                          long long n, int s, int S, double2 sh) {
-  const long long slot = (long long)A * g.Nn + n;
-  const double m = __ldg(mass + slot);
-  double2 out = tem::czero();
-  if (m > 0.0) {
-    int pos[3];
-    tem::node_pos(g, n, pos);
-    const tem::EdgeWeights w = tem::edge_weights<A>(g, pos);
-    const double2 a0 = __ldg(x + slot * S + s);
-    out = tem::curlcurl<A>(g, x, n, s, S, w, a0);
-    out = tem::cfma(sh, tem::cscale(m, a0), out);
-  }
-  y[slot * S + s] = out;
+__device__ __forceinline__ double kdiag(const Grid& g, int a, const int pos[3]) {
+  if (a == 0) return tem::edge_weights<0>(g, pos).diag();
+  if (a == 1) return tem::edge_weights<1>(g, pos).diag();
+  return tem::edge_weights<2>(g, pos).diag();
 }
 
-__global__ void k_apply(Grid g, int S, int tile_nodes, long long ntiles, ShiftList sl,
-                        const double* __restrict__ mass, const double2* __restrict__ x,
-                        double2* __restrict__ y) {
-  const int s = threadIdx.x % S;
-  const int nl = threadIdx.x / S;
-  if (nl >= tile_nodes) return;
-  const double2 sh = sl.s[s];
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int a = (int)(t % 3);
-    const long long n = (t / 3) * tile_nodes + nl;
-    if (n >= g.Nn) continue;
-    if (a == 0) apply_one<0>(g, mass, x, y, n, s, S, sh);
-    else if (a == 1) apply_one<1>(g, mass, x, y, n, s, S, sh);
-    else apply_one<2>(g, mass, x, y, n, s, S, sh);
-  }
-}
-
-// COCG init: x = 0, p = 0, r = f, rho = r^T D^-1 r, ||f||.
-__global__ void k_init(SolveArgs A) {
-  extern __shared__ unsigned char smem_raw[];
-  double* buf = reinterpret_cast<double*>(smem_raw);
+// COCG init (z-form): x = 0, p0 = p1 = 0, z = D^-1 f; rho = f^T z, ||f||^2.
+// Block b serves shift b % S.
+__global__ void __launch_bounds__(256) k_init(tem::SweepArgs A, double2* p0, double2* p1,
+                                              const double* __restrict__ f) {
+  __shared__ double red[3 * 8];
   const Grid& g = A.g;
   const int S = A.S;
-  const int s = threadIdx.x % S;
-  const int nl = threadIdx.x / S;
-  const bool lane_ok = nl < A.tile_nodes;
+  const int s = blockIdx.x % S;
+  const int nb = gridDim.x / S;
+  const int b = blockIdx.x / S;
   const double2 sh = A.st[s].s;
+  const long long vs = (long long)s * 3 * g.Nn;
   double2 rho = tem::czero();
   double rr = 0.0;
-  for (long long t = blockIdx.x; t < A.ntiles; t += gridDim.x) {
-    const int a = (int)(t % 3);
-    const long long n = (t / 3) * A.tile_nodes + nl;
-    if (!lane_ok || n >= g.Nn) continue;
-    const long long slot = (long long)a * g.Nn + n;
-    const long long e = slot * S + s;
+  for (long long slot = b * 256LL + threadIdx.x; slot < 3 * g.Nn; slot += (long long)nb * 256) {
     const double m = __ldg(A.mass + slot);
-    double2 r0 = tem::czero();
+    double2 zv = tem::czero();
     if (m > 0.0) {
-      r0 = make_double2(__ldg(A.f + slot), 0.0);
+      const int a = (int)(slot / g.Nn);
       int pos[3];
-      tem::node_pos(g, n, pos);
-      double kd;
-      if (a == 0) kd = tem::edge_weights<0>(g, pos).diag();
-      else if (a == 1) kd = tem::edge_weights<1>(g, pos).diag();
-      else kd = tem::edge_weights<2>(g, pos).diag();
-      const double2 D = make_double2(kd + m * sh.x, m * sh.y);
-      rho += tem::cmul(r0, tem::cdiv(r0, D));
-      rr += r0.x * r0.x;
+      tem::node_pos(g, slot - a * g.Nn, pos);
+      const double2 D = make_double2(kdiag(g, a, pos) + m * sh.x, m * sh.y);
+      const double fv = __ldg(f + slot);
+      zv = tem::cdiv(make_double2(fv, 0.0), D);
+      rho = tem::cfma(make_double2(fv, 0.0), zv, rho);
+      rr += fv * fv;
     }
-    A.x[e] = tem::czero();
-    A.p[e] = tem::czero();
-    A.r[e] = r0;
+    A.x[vs + slot] = tem::czero();
+    A.z[vs + slot] = zv;
+    p0[vs + slot] = tem::czero();
+    p1[vs + slot] = tem::czero();
   }
-  // per-shift block sums -> partials
-  double2* bufc = reinterpret_cast<double2*>(smem_raw);
-  const double2 bc = block_sum_per_shift<double2>(lane_ok ? rho : tem::czero(), bufc, S, A.tile_nodes);
-  const double br = block_sum_per_shift<double>(lane_ok ? rr : 0.0, buf, S, A.tile_nodes);
-  if ((int)threadIdx.x < S) {
-    A.part_c[blockIdx.x * S + threadIdx.x] = bc;
-    A.part_r[blockIdx.x * S + threadIdx.x] = br;
+  tem::block_sum_n<256>(rho, rr, red);
+  if (threadIdx.x == 0) {
+    A.part_c[blockIdx.x] = rho;
+    A.part_r[blockIdx.x] = rr;
   }
-  if (!last_block(&A.ctl->ticket[0])) return;
-  // only full warps take part (blockDim may not be a multiple of 32)
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
-  for (int q = warp; warp < nw && q < S; q += nw) {
+  if (!tem::last_block(&A.ctl->ticket[0])) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int q = warp; q < S; q += 8) {
     double cx = 0, cy = 0, cr = 0;
-    for (int b = lane; b < (int)gridDim.x; b += 32) {
-      const double2 v = __ldcg(A.part_c + b * S + q);
+    for (int bb = q + lane * S; bb < (int)gridDim.x; bb += 32 * S) {
+      const double2 v = __ldcg(A.part_c + bb);
       cx += v.x;
       cy += v.y;
-      cr += __ldcg(A.part_r + b * S + q);
+      cr += __ldcg(A.part_r + bb);
     }
-    cx = warp_sum(cx);
-    cy = warp_sum(cy);
-    cr = warp_sum(cr);
+    cx = tem::warp_sum(cx);
+    cy = tem::warp_sum(cy);
+    cr = tem::warp_sum(cr);
     if (lane == 0) {
-      ShiftState& st = A.st[q];
+      tem::ShiftState& st = A.st[q];
       st.rho = make_double2(cx, cy);
       st.fnorm = sqrt(cr);
       st.relres = cr > 0 ? 1.0 : 0.0;
@@ -284,209 +165,7 @@ __global__ void k_init(SolveArgs A) {
   }
 }
 
-// p = D^-1 r + beta p  (elementwise; active shifts only)
-template <int AX>
-__device__ __forceinline__ void dir_one(const SolveArgs& A, long long n, int s, double2 sh, double2 beta) {
-  const Grid& g = A.g;
-  const long long slot = (long long)AX * g.Nn + n;
-  const double m = __ldg(A.mass + slot);
-  if (m <= 0.0) return;
-  int pos[3];
-  tem::node_pos(g, n, pos);
-  const double kd = tem::edge_weights<AX>(g, pos).diag();
-  const double2 D = make_double2(kd + m * sh.x, m * sh.y);
-  const long long e = slot * A.S + s;
-  const double2 z = tem::cdiv(A.r[e], D);
-  A.p[e] = tem::cfma(beta, A.p[e], z);
-}
-
-__global__ void k_dir(SolveArgs A) {
-  if (A.ctl->n_active == 0) return;
-  const int S = A.S;
-  const int s = threadIdx.x % S;
-  const int nl = threadIdx.x / S;
-  if (nl >= A.tile_nodes) return;
-  const ShiftState st = A.st[s];
-  if (!st.active) return;
-  for (long long t = blockIdx.x; t < A.ntiles; t += gridDim.x) {
-    const int a = (int)(t % 3);
-    const long long n = (t / 3) * A.tile_nodes + nl;
-    if (n >= A.g.Nn) continue;
-    if (a == 0) dir_one<0>(A, n, s, st.s, st.beta);
-    else if (a == 1) dir_one<1>(A, n, s, st.s, st.beta);
-    else dir_one<2>(A, n, s, st.s, st.beta);
-  }
-}
-
-// mu partial: p^T (A p)
-template <int AX>
-__device__ __forceinline__ double2 ap_one(const SolveArgs& A, long long n, int s, double2 sh) {
-  const Grid& g = A.g;
-  const long long slot = (long long)AX * g.Nn + n;
-  const double m = __ldg(A.mass + slot);
-  if (m <= 0.0) return tem::czero();
-  int pos[3];
-  tem::node_pos(g, n, pos);
-  const tem::EdgeWeights w = tem::edge_weights<AX>(g, pos);
-  const double2 p0 = __ldg(A.p + slot * A.S + s);
-  double2 q = tem::curlcurl<AX>(g, A.p, n, s, A.S, w, p0);
-  q = tem::cfma(sh, tem::cscale(m, p0), q);
-  return tem::cmul(p0, q);
-}
-
-__global__ void k_ap(SolveArgs A) {
-  extern __shared__ unsigned char smem_raw[];
-  if (A.ctl->n_active == 0) return;
-  const int S = A.S;
-  const int s = threadIdx.x % S;
-  const int nl = threadIdx.x / S;
-  const bool lane_ok = nl < A.tile_nodes;
-  const ShiftState st = A.st[s];
-  double2 mu = tem::czero();
-  if (lane_ok && st.active) {
-    for (long long t = blockIdx.x; t < A.ntiles; t += gridDim.x) {
-      const int a = (int)(t % 3);
-      const long long n = (t / 3) * A.tile_nodes + nl;
-      if (n >= A.g.Nn) continue;
-      if (a == 0) mu += ap_one<0>(A, n, s, st.s);
-      else if (a == 1) mu += ap_one<1>(A, n, s, st.s);
-      else mu += ap_one<2>(A, n, s, st.s);
-    }
-  }
-  double2* bufc = reinterpret_cast<double2*>(smem_raw);
-  const double2 bc = block_sum_per_shift<double2>(mu, bufc, S, A.tile_nodes);
-  if ((int)threadIdx.x < S) A.part_c[blockIdx.x * S + threadIdx.x] = bc;
-  if (!last_block(&A.ctl->ticket[1])) return;
-  // only full warps take part (blockDim may not be a multiple of 32)
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
-  for (int q = warp; warp < nw && q < S; q += nw) {
-    if (!A.st[q].active) continue;
-    double cx = 0, cy = 0;
-    for (int b = lane; b < (int)gridDim.x; b += 32) {
-      const double2 v = __ldcg(A.part_c + b * S + q);
-      cx += v.x;
-      cy += v.y;
-    }
-    cx = warp_sum(cx);
-    cy = warp_sum(cy);
-    if (lane == 0) {
-      ShiftState& sq = A.st[q];
-      const double2 mu_q = make_double2(cx, cy);
-      if (mu_q.x == 0.0 && mu_q.y == 0.0) {
-        sq.status = 2;  // breakdown
-        sq.active = 0;
-        sq.alpha = tem::czero();
-      } else {
-        sq.alpha = tem::cdiv(sq.rho, mu_q);
-      }
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int na = 0;
-    for (int q = 0; q < S; ++q) na += A.st[q].active;
-    A.ctl->n_active = na;
-    A.ctl->ticket[1] = 0;
-  }
-}
-
-// x += alpha p ; r -= alpha A p ; rho' = r^T D^-1 r ; rr = ||r||^2
-template <int AX>
-__device__ __forceinline__ void upd_one(const SolveArgs& A, long long n, int s, double2 sh,
-                                        double2 alpha, double2& rho, double& rr) {
-  const Grid& g = A.g;
-  const long long slot = (long long)AX * g.Nn + n;
-  const double m = __ldg(A.mass + slot);
-  if (m <= 0.0) return;
-  int pos[3];
-  tem::node_pos(g, n, pos);
-  const tem::EdgeWeights w = tem::edge_weights<AX>(g, pos);
-  const long long e = slot * A.S + s;
-  const double2 p0 = __ldg(A.p + e);
-  double2 q = tem::curlcurl<AX>(g, A.p, n, s, A.S, w, p0);
-  q = tem::cfma(sh, tem::cscale(m, p0), q);
-  A.x[e] = tem::cfma(alpha, p0, A.x[e]);
-  const double2 r = tem::cfma(make_double2(-alpha.x, -alpha.y), q, A.r[e]);
-  A.r[e] = r;
-  const double2 D = make_double2(w.diag() + m * sh.x, m * sh.y);
-  rho += tem::cmul(r, tem::cdiv(r, D));
-  rr += r.x * r.x + r.y * r.y;
-}
-
-__global__ void k_upd(SolveArgs A) {
-  extern __shared__ unsigned char smem_raw[];
-  if (A.ctl->n_active == 0) return;
-  const int S = A.S;
-  const int s = threadIdx.x % S;
-  const int nl = threadIdx.x / S;
-  const bool lane_ok = nl < A.tile_nodes;
-  const ShiftState st = A.st[s];
-  double2 rho = tem::czero();
-  double rr = 0.0;
-  if (lane_ok && st.active) {
-    for (long long t = blockIdx.x; t < A.ntiles; t += gridDim.x) {
-      const int a = (int)(t % 3);
-      const long long n = (t / 3) * A.tile_nodes + nl;
-      if (n >= A.g.Nn) continue;
-      if (a == 0) upd_one<0>(A, n, s, st.s, st.alpha, rho, rr);
-      else if (a == 1) upd_one<1>(A, n, s, st.s, st.alpha, rho, rr);
-      else upd_one<2>(A, n, s, st.s, st.alpha, rho, rr);
-    }
-  }
-  double2* bufc = reinterpret_cast<double2*>(smem_raw);
-  double* bufr = reinterpret_cast<double*>(smem_raw);
-  const double2 bc = block_sum_per_shift<double2>(rho, bufc, S, A.tile_nodes);
-  const double br = block_sum_per_shift<double>(rr, bufr, S, A.tile_nodes);
-  if ((int)threadIdx.x < S) {
-    A.part_c[blockIdx.x * S + threadIdx.x] = bc;
-    A.part_r[blockIdx.x * S + threadIdx.x] = br;
-  }
-  if (!last_block(&A.ctl->ticket[2])) return;
-  // only full warps take part (blockDim may not be a multiple of 32)
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
-  for (int q = warp; warp < nw && q < S; q += nw) {
-    if (!A.st[q].active) continue;
-    double cx = 0, cy = 0, cr = 0;
-    for (int b = lane; b < (int)gridDim.x; b += 32) {
-      const double2 v = __ldcg(A.part_c + b * S + q);
-      cx += v.x;
-      cy += v.y;
-      cr += __ldcg(A.part_r + b * S + q);
-    }
-    cx = warp_sum(cx);
-    cy = warp_sum(cy);
-    cr = warp_sum(cr);
-    if (lane == 0) {
-      ShiftState& sq = A.st[q];
-      const double2 rho_new = make_double2(cx, cy);
-      sq.iters += 1;
-      sq.relres = sqrt(cr) / sq.fnorm;
-      if (sq.relres <= A.ctl->tol) {
-        sq.active = 0;
-        sq.status = 1;
-      } else if (sq.rho.x == 0.0 && sq.rho.y == 0.0) {
-        sq.active = 0;
-        sq.status = 2;
-      } else {
-        sq.beta = tem::cdiv(rho_new, sq.rho);
-        sq.rho = rho_new;
-        if (rho_new.x == 0.0 && rho_new.y == 0.0) {
-          sq.active = 0;
-          sq.status = 2;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int na = 0;
-    for (int q = 0; q < S; ++q) na += A.st[q].active;
-    A.ctl->n_active = na;
-    A.ctl->ticket[2] = 0;
-  }
-}
-
-// u[k][slot] = sum_s w_s Re(res[k][s] x[slot][s]); 0 on non-free slots.
+// u[k][slot] = sum_s w_s Re(res[k][s] x[s][slot]); 0 on non-free slots.
 __device__ __forceinline__ bool free_slot(const Grid& g, long long slot) {
   const int a = (int)(slot / g.Nn);
   int pos[3];
@@ -515,7 +194,7 @@ __global__ void k_synth(Grid g, int S, int K, const double2* __restrict__ res,
     double2 xv[SMAX];
 #pragma unroll
     for (int s = 0; s < SMAX; ++s)
-      xv[s] = (live && s < S) ? __ldg(x + slot * S + s) : tem::czero();
+      xv[s] = (live && s < S) ? __ldg(x + (long long)s * nslots + slot) : tem::czero();
     for (int k = 0; k < K; ++k) {
       double acc = 0.0;
 #pragma unroll
@@ -541,11 +220,9 @@ struct tem_ctx {
   double* dev_h = nullptr;          // ih[3] and hdm[3] packed
   cudaStream_t cap_stream = nullptr;
   int* pinned_active = nullptr;
-  // cached graph
+  // cached graph of kChunk COCG iterations
   cudaGraphExec_t graph = nullptr;
-  SolveArgs graph_args{};
-  int graph_grid = 0, graph_block = 0;
-  size_t graph_smem = 0;
+  tem::SweepArgs graph_a1{}, graph_a2{};
   // scratch
   void* scratch = nullptr;          // residues etc.
   size_t scratch_bytes = 0;
@@ -556,17 +233,44 @@ struct tem_ctx {
   tem_solve_stats stats{};
 };
 
-static int tile_nodes_for(int S) { return std::max(1, kTargetThreads / S); }
-
 static int check_S(int S) {
   if (S < 1 || S > TEM_MAX_SHIFTS)
     return fail(TEM_EINVAL, "S must be in [1, " + std::to_string(TEM_MAX_SHIFTS) + "]");
   return TEM_OK;
 }
 
+static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// sweep geometry: xy tiles x z-chunks x shifts
+static void sweep_geometry(const tem_ctx* c, int S, tem::SweepArgs& A, int* grid) {
+  A.g = c->g;
+  A.S = S;
+  A.ntx = (c->g.n[0] + tem::TX - 1) / tem::TX;
+  A.nty = (c->g.n[1] + tem::TY - 1) / tem::TY;
+  // split z so that the grid covers the machine several times over
+  const int per_wave = c->num_sms * 3;
+  const int base = A.ntx * A.nty * S;
+  int nzc = 1;
+  while (base * nzc < 4 * per_wave && c->g.n[2] / (nzc * 2) >= 16) nzc *= 2;
+  A.nzc = nzc;
+  A.kchunk = (c->g.n[2] + nzc - 1) / nzc;
+  A.nzc = (c->g.n[2] + A.kchunk - 1) / A.kchunk;
+  *grid = A.ntx * A.nty * A.nzc * S;
+}
+
+static int sweep_attrs() {
+  static bool done = false;
+  if (done) return TEM_OK;
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSweepSmem));
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSweepSmem));
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSweepSmem));
+  done = true;
+  return TEM_OK;
+}
+
 extern "C" {
 
-const char* tem_version(void) { return "tem_b200 0.1 sm_100a"; }
+const char* tem_version(void) { return "tem_b200 0.2 sm_100a"; }
 const char* tem_last_error(void) { return g_last_error.c_str(); }
 
 int tem_create(int nx, int ny, int nz, const double* hx, const double* hy, const double* hz,
@@ -574,6 +278,9 @@ int tem_create(int nx, int ny, int nz, const double* hx, const double* hy, const
   if (!out || !hx || !hy || !hz) return fail(TEM_EINVAL, "tem_create: null pointer");
   *out = nullptr;
   if (nx < 2 || ny < 2 || nz < 2) return fail(TEM_EINVAL, "tem_create: need nx, ny, nz >= 2");
+  const long long Nn = (long long)(nx + 1) * (ny + 1) * (nz + 1);
+  if (Nn * 3 * TEM_MAX_SHIFTS >= (1LL << 40))
+    return fail(TEM_EINVAL, "tem_create: grid too large");
   const int n[3] = {nx, ny, nz};
   const double* h[3] = {hx, hy, hz};
   for (int a = 0; a < 3; ++a)
@@ -586,7 +293,7 @@ int tem_create(int nx, int ny, int nz, const double* hx, const double* hy, const
   c->g.st[0] = 1;
   c->g.st[1] = nx + 1;
   c->g.st[2] = (long long)(nx + 1) * (ny + 1);
-  c->g.Nn = (long long)(nx + 1) * (ny + 1) * (nz + 1);
+  c->g.Nn = Nn;
   // host tables: 1/h and hdual/mu0
   std::vector<double> tab;
   size_t off_ih[3], off_hd[3];
@@ -617,6 +324,10 @@ int tem_create(int nx, int ny, int nz, const double* hx, const double* hy, const
   for (int a = 0; a < 3; ++a) {
     c->g.ih[a] = c->dev_h + off_ih[a];
     c->g.hdm[a] = c->dev_h + off_hd[a];
+  }
+  if (int rc = sweep_attrs()) {
+    tem_destroy(c);
+    return rc;
   }
   *out = c;
   return TEM_OK;
@@ -655,38 +366,38 @@ int tem_apply_shifted(tem_ctx* c, const double* mass, int S, const double* shift
                       const double* x, double* y, void* stream) {
   if (!c || !mass || !shifts || !x || !y) return fail(TEM_EINVAL, "tem_apply_shifted: null pointer");
   if (int rc = check_S(S)) return rc;
-  ShiftList sl{};
-  for (int s = 0; s < S; ++s) sl.s[s] = make_double2(shifts[2 * s], shifts[2 * s + 1]);
-  const int tn = tile_nodes_for(S);
-  const long long ntiles = 3 * ((c->g.Nn + tn - 1) / tn);
-  const int block = tn * S;
-  const int grid = (int)std::min<long long>(ntiles, (long long)c->num_sms * 8);
-  // zero y first so slots never visited by a thread (tile padding) are 0
+  tem::SweepArgs A{};
+  int grid = 0;
+  sweep_geometry(c, S, A, &grid);
+  for (int s = 0; s < S; ++s) A.shifts[s] = make_double2(shifts[2 * s], shifts[2 * s + 1]);
+  A.mass = mass;
+  A.v = reinterpret_cast<const double2*>(x);
+  A.out = reinterpret_cast<double2*>(y);
   TEM_CUDA(cudaMemsetAsync(y, 0, (size_t)3 * c->g.Nn * S * sizeof(double2), (cudaStream_t)stream));
-  k_apply<<<grid, block, 0, (cudaStream_t)stream>>>(c->g, S, tn, ntiles, sl, mass,
-                                                    reinterpret_cast<const double2*>(x),
-                                                    reinterpret_cast<double2*>(y));
+  tem::k_sweep<0><<<grid, tem::NT, tem::kSweepSmem, (cudaStream_t)stream>>>(A);
   TEM_CUDA(cudaGetLastError());
   return TEM_OK;
 }
 
-static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
-
 struct WorkLayout {
-  size_t r, p, st, ctl, part_c, part_r, total;
+  size_t z, p0, p1, st, ctl, part_c, part_r, total;
 };
 
 static WorkLayout work_layout(const tem_ctx* c, int S) {
   WorkLayout L{};
   const size_t vec = (size_t)3 * c->g.Nn * S * sizeof(double2);
-  const size_t maxgrid = (size_t)c->num_sms * kMaxGridMult;
+  tem::SweepArgs A{};
+  int grid = 0;
+  sweep_geometry(c, S, A, &grid);
+  const size_t nparts = (size_t)std::max(grid, 1024 * S);
   size_t o = 0;
-  L.r = o;      o = align_up(o + vec, 256);
-  L.p = o;      o = align_up(o + vec, 256);
-  L.st = o;     o = align_up(o + sizeof(ShiftState) * TEM_MAX_SHIFTS, 256);
-  L.ctl = o;    o = align_up(o + sizeof(Control), 256);
-  L.part_c = o; o = align_up(o + maxgrid * S * sizeof(double2), 256);
-  L.part_r = o; o = align_up(o + maxgrid * S * sizeof(double), 256);
+  L.z = o;      o = align_up(o + vec, 256);
+  L.p0 = o;     o = align_up(o + vec, 256);
+  L.p1 = o;     o = align_up(o + vec, 256);
+  L.st = o;     o = align_up(o + sizeof(tem::ShiftState) * TEM_MAX_SHIFTS, 256);
+  L.ctl = o;    o = align_up(o + sizeof(tem::Control), 256);
+  L.part_c = o; o = align_up(o + nparts * sizeof(double2), 256);
+  L.part_r = o; o = align_up(o + nparts * sizeof(double), 256);
   L.total = o;
   return L;
 }
@@ -696,11 +407,10 @@ size_t tem_cocg_workspace_bytes(const tem_ctx* c, int S) {
   return work_layout(c, S).total;
 }
 
-static int solve_grid(const tem_ctx* c, int block, size_t smem, const void* kern) {
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, smem);
-  per_sm = std::max(1, std::min(per_sm, kMaxGridMult));
-  return c->num_sms * per_sm;
+static bool same_args(const tem::SweepArgs& a, const tem::SweepArgs& b) {
+  return a.S == b.S && a.mass == b.mass && a.v == b.v && a.zin == b.zin && a.out == b.out &&
+         a.x == b.x && a.z == b.z && a.st == b.st && a.ctl == b.ctl && a.part_c == b.part_c &&
+         a.part_r == b.part_r && a.g.Nn == b.g.Nn && a.g.ih[0] == b.g.ih[0] && a.nzc == b.nzc;
 }
 
 int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const double* shifts,
@@ -714,51 +424,49 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
   cudaStream_t stream = (cudaStream_t)stream_;
   char* w = static_cast<char*>(work);
 
-  SolveArgs A{};
-  A.g = c->g;
-  A.S = S;
-  A.tile_nodes = tile_nodes_for(S);
-  A.ntiles = 3 * ((c->g.Nn + A.tile_nodes - 1) / A.tile_nodes);
-  A.mass = mass;
-  A.f = f;
-  A.x = reinterpret_cast<double2*>(x);
-  A.r = reinterpret_cast<double2*>(w + L.r);
-  A.p = reinterpret_cast<double2*>(w + L.p);
-  A.st = reinterpret_cast<ShiftState*>(w + L.st);
-  A.ctl = reinterpret_cast<Control*>(w + L.ctl);
-  A.part_c = reinterpret_cast<double2*>(w + L.part_c);
-  A.part_r = reinterpret_cast<double*>(w + L.part_r);
-  const int block = A.tile_nodes * S;
-  const size_t smem = (size_t)block * sizeof(double2);
-  int grid = solve_grid(c, block, smem, (const void*)k_upd);
-  grid = (int)std::min<long long>(grid, A.ntiles);
+  tem::SweepArgs base{};
+  int grid = 0;
+  sweep_geometry(c, S, base, &grid);
+  base.mass = mass;
+  base.x = reinterpret_cast<double2*>(x);
+  base.z = reinterpret_cast<double2*>(w + L.z);
+  base.st = reinterpret_cast<tem::ShiftState*>(w + L.st);
+  base.ctl = reinterpret_cast<tem::Control*>(w + L.ctl);
+  base.part_c = reinterpret_cast<double2*>(w + L.part_c);
+  base.part_r = reinterpret_cast<double*>(w + L.part_r);
+  double2* P[2] = {reinterpret_cast<double2*>(w + L.p0), reinterpret_cast<double2*>(w + L.p1)};
+  // iteration parity q: sweep 1 reads p_old = P[q], writes p_new = P[1-q]; sweep 2 reads P[1-q]
+  tem::SweepArgs a1[2], a2[2];
+  for (int q = 0; q < 2; ++q) {
+    a1[q] = base;
+    a1[q].v = P[q];
+    a1[q].zin = base.z;
+    a1[q].out = P[1 - q];
+    a2[q] = base;
+    a2[q].v = P[1 - q];
+  }
 
   // per-shift state + control (host -> device, small)
-  std::vector<ShiftState> st(S);
+  std::vector<tem::ShiftState> st(S);
   for (int s = 0; s < S; ++s) {
-    memset(&st[s], 0, sizeof(ShiftState));
+    memset(&st[s], 0, sizeof(tem::ShiftState));
     st[s].s = make_double2(shifts[2 * s], shifts[2 * s + 1]);
   }
-  Control ctl{};
+  tem::Control ctl{};
   ctl.tol = tol;
-  TEM_CUDA(cudaMemcpyAsync(A.st, st.data(), sizeof(ShiftState) * S, cudaMemcpyHostToDevice, stream));
-  TEM_CUDA(cudaMemcpyAsync(A.ctl, &ctl, sizeof(Control), cudaMemcpyHostToDevice, stream));
+  TEM_CUDA(cudaMemcpyAsync(base.st, st.data(), sizeof(tem::ShiftState) * S, cudaMemcpyHostToDevice, stream));
+  TEM_CUDA(cudaMemcpyAsync(base.ctl, &ctl, sizeof(tem::Control), cudaMemcpyHostToDevice, stream));
 
   cudaEvent_t ev0, ev1;
   TEM_CUDA(cudaEventCreate(&ev0));
   TEM_CUDA(cudaEventCreate(&ev1));
   TEM_CUDA(cudaEventRecord(ev0, stream));
-  k_init<<<grid, block, smem, stream>>>(A);
+  const int init_grid = S * std::max(1, std::min(64, (int)((3 * c->g.Nn + 255) / 256)));
+  k_init<<<init_grid, 256, 0, stream>>>(base, P[0], P[1], f);
   TEM_CUDA(cudaGetLastError());
   long long launches = 1;
 
-  // (re)build the cached graph of kChunk iterations if the arguments changed
-  const SolveArgs& G = c->graph_args;
-  const bool same = c->graph && c->graph_grid == grid && c->graph_block == block &&
-                    G.S == A.S && G.mass == A.mass && G.f == A.f && G.x == A.x &&
-                    G.r == A.r && G.p == A.p && G.st == A.st && G.ctl == A.ctl &&
-                    G.part_c == A.part_c && G.part_r == A.part_r && G.g.Nn == A.g.Nn &&
-                    G.g.ih[0] == A.g.ih[0];
+  const bool same = c->graph && same_args(c->graph_a1, a1[0]) && same_args(c->graph_a2, a2[0]);
   if (!same) {
     if (c->graph) {
       cudaGraphExecDestroy(c->graph);
@@ -767,41 +475,38 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
     cudaGraph_t gr;
     TEM_CUDA(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
     for (int it = 0; it < kChunk; ++it) {
-      k_dir<<<grid, block, 0, c->cap_stream>>>(A);
-      k_ap<<<grid, block, smem, c->cap_stream>>>(A);
-      k_upd<<<grid, block, smem, c->cap_stream>>>(A);
+      tem::k_sweep<1><<<grid, tem::NT, tem::kSweepSmem, c->cap_stream>>>(a1[it & 1]);
+      tem::k_sweep<2><<<grid, tem::NT, tem::kSweepSmem, c->cap_stream>>>(a2[it & 1]);
     }
     TEM_CUDA(cudaStreamEndCapture(c->cap_stream, &gr));
     cudaError_t e = cudaGraphInstantiate(&c->graph, gr, 0);
     cudaGraphDestroy(gr);
     if (e != cudaSuccess) return fail(TEM_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
-    c->graph_args = A;
-    c->graph_grid = grid;
-    c->graph_block = block;
+    c->graph_a1 = a1[0];
+    c->graph_a2 = a2[0];
   }
   int done = 0;
   int n_active = S;
   while (done < maxit) {
     const int chunk = std::min(kChunk, maxit - done);
-    if (chunk == kChunk) {
+    if (chunk == kChunk) {  // kChunk is even: parity returns to 0
       TEM_CUDA(cudaGraphLaunch(c->graph, stream));
     } else {
       for (int it = 0; it < chunk; ++it) {
-        k_dir<<<grid, block, 0, stream>>>(A);
-        k_ap<<<grid, block, smem, stream>>>(A);
-        k_upd<<<grid, block, smem, stream>>>(A);
+        tem::k_sweep<1><<<grid, tem::NT, tem::kSweepSmem, stream>>>(a1[(done + it) & 1]);
+        tem::k_sweep<2><<<grid, tem::NT, tem::kSweepSmem, stream>>>(a2[(done + it) & 1]);
       }
       TEM_CUDA(cudaGetLastError());
     }
-    launches += 3LL * chunk;
+    launches += 2LL * chunk;
     done += chunk;
-    TEM_CUDA(cudaMemcpyAsync(c->pinned_active, &A.ctl->n_active, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    TEM_CUDA(cudaMemcpyAsync(c->pinned_active, &base.ctl->n_active, sizeof(int), cudaMemcpyDeviceToHost, stream));
     TEM_CUDA(cudaStreamSynchronize(stream));
     n_active = *c->pinned_active;
     if (n_active == 0) break;
   }
   TEM_CUDA(cudaEventRecord(ev1, stream));
-  TEM_CUDA(cudaMemcpyAsync(st.data(), A.st, sizeof(ShiftState) * S, cudaMemcpyDeviceToHost, stream));
+  TEM_CUDA(cudaMemcpyAsync(st.data(), base.st, sizeof(tem::ShiftState) * S, cudaMemcpyDeviceToHost, stream));
   TEM_CUDA(cudaStreamSynchronize(stream));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ev0, ev1);
@@ -824,7 +529,7 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
   c->stats.shift_iterations = shift_iters;
   c->stats.iterations = max_it;
   c->stats.grid = grid;
-  c->stats.block = block;
+  c->stats.block = tem::NT;
   if (status == TEM_EBREAKDOWN) return fail(status, "tem_cocg_solve: COCG breakdown");
   if (status == TEM_ENOCONV) return fail(status, "tem_cocg_solve: not converged within maxit");
   return TEM_OK;

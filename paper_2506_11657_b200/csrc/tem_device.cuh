@@ -10,7 +10,9 @@
 //   C_b(m') = u_d(m') + u_a(m'+e_d) - u_d(m'+e_a) - u_a(m')
 // and W_d(m') = hdual_d[m'_d] / (mu0 h_a[m'_a] h_b[m'_b]).  This is
 // K = T^T W T (§2.2 [K]_ij = (mu^-1 curl Phi_j, curl Phi_i)) written
-// as a 13-point gather; nothing is assembled.
+// as a 13-point gather; nothing is assembled.  The gather itself lives in
+// tem_sweep.cuh (shared-memory plane ring); this header holds the grid,
+// complex helpers and the per-edge face weights.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -62,33 +64,6 @@ __device__ __forceinline__ EdgeWeights edge_weights(const Grid& g, const int pos
   w.wb0 = hdB * iha * __ldg(g.ih[D] + pos[D]);
   w.wb1 = hdB * iha * __ldg(g.ih[D] + pos[D] - 1);
   return w;
-}
-
-// (K v)_A at node n for shift lane s of a complex shift block v[3][Nn][S].
-// Only called for free edges (all 12 neighbours exist and non-free ones hold 0).
-template <int A>
-__device__ __forceinline__ double2 curlcurl(const Grid& g, const double2* __restrict__ v,
-                                            long long n, int s, int S, const EdgeWeights& w,
-                                            double2 a0) {
-  constexpr int B = (A + 1) % 3, D = (A + 2) % 3;
-  const long long sA = g.st[A], sB = g.st[B], sD = g.st[D];
-  const double2* va = v + (long long)A * g.Nn * S + s;
-  const double2* vb = v + (long long)B * g.Nn * S + s;
-  const double2* vd = v + (long long)D * g.Nn * S + s;
-#define TEM_LD(arr, node) __ldg((arr) + (node) * S)
-  // face normal to D at m and at m - e_B
-  const double2 cD0 = csub(cadd(a0, TEM_LD(vb, n + sA)), cadd(TEM_LD(va, n + sB), TEM_LD(vb, n)));
-  const double2 cD1 = csub(cadd(TEM_LD(va, n - sB), TEM_LD(vb, n - sB + sA)),
-                           cadd(a0, TEM_LD(vb, n - sB)));
-  // face normal to B at m and at m - e_D
-  const double2 cB0 = csub(cadd(TEM_LD(vd, n), TEM_LD(va, n + sD)), cadd(TEM_LD(vd, n + sA), a0));
-  const double2 cB1 = csub(cadd(TEM_LD(vd, n - sD), a0),
-                           cadd(TEM_LD(vd, n - sD + sA), TEM_LD(va, n - sD)));
-#undef TEM_LD
-  double2 r;
-  r.x = w.wd0 * cD0.x - w.wd1 * cD1.x - w.wb0 * cB0.x + w.wb1 * cB1.x;
-  r.y = w.wd0 * cD0.y - w.wd1 * cD1.y - w.wb0 * cB0.y + w.wb1 * cB1.y;
-  return r;
 }
 
 __device__ __forceinline__ void node_pos(const Grid& g, long long n, int pos[3]) {

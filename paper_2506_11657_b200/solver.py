@@ -150,12 +150,12 @@ class TemForward:
         return mass
 
     def apply(self, mass: torch.Tensor, shifts, x: torch.Tensor, stream=None) -> torch.Tensor:
-        """y[:, s] = (K + s M) x[:, s]; x is complex128 (n_slots, S)."""
+        """y[s] = (K + s M) x[s]; x is complex128 (S, n_slots), non-free slots 0."""
         sh = _cplx(shifts)
         S = sh.size // 2
         _need_cuda(x, torch.complex128, "x")
-        if x.shape != (self.n_slots, S):
-            raise ValueError(f"x must be (n_slots, S) = {(self.n_slots, S)}")
+        if x.shape != (S, self.n_slots):
+            raise ValueError(f"x must be (S, n_slots) = {(S, self.n_slots)}")
         y = torch.empty_like(x)
         _lib.check(self.lib.tem_apply_shifted(self._h, ctypes.c_void_p(mass.data_ptr()), S,
                                               _dptr(sh), ctypes.c_void_p(x.data_ptr()),
@@ -177,7 +177,7 @@ class TemForward:
         sh = _cplx(shifts)
         S = sh.size // 2
         if x is None:
-            x = torch.empty((self.n_slots, S), dtype=torch.complex128, device=self.device)
+            x = torch.empty((S, self.n_slots), dtype=torch.complex128, device=self.device)
         work = self.workspace(S)
         iters = np.zeros(S, dtype=np.int32)
         relres = np.zeros(S, dtype=np.float64)
@@ -196,11 +196,11 @@ class TemForward:
         return {k: getattr(st, k) for k, _ in _lib.SolveStats._fields_}
 
     def synthesize(self, x: torch.Tensor, residues, is_pair, stream=None) -> torch.Tensor:
-        """u[k] = sum_s w_s Re(residues[s, k] x[:, s]); residues (S, K)."""
+        """u[k] = sum_s w_s Re(residues[s, k] x[s]); residues (S, K), x (S, n_slots)."""
         res = np.asarray(residues, dtype=np.complex128)
         S, K = res.shape
         _need_cuda(x, torch.complex128, "x")
-        if x.shape != (self.n_slots, S):
+        if x.shape != (S, self.n_slots):
             raise ValueError("x shape mismatch")
         r = _cplx(res.T.copy())           # ABI wants [K][S]
         ip = np.ascontiguousarray(np.asarray(is_pair, dtype=np.int32))

@@ -75,17 +75,17 @@ def test_apply_shifted(name, S):
     rng = np.random.default_rng(S)
     shifts = (10 ** rng.uniform(1, 6, S)) * np.exp(1j * rng.uniform(-np.pi, np.pi, S))
     X = rng.normal(size=(asm.n, S)) + 1j * rng.normal(size=(asm.n, S))
-    xg = np.zeros((fw.n_slots, S), dtype=np.complex128)
-    xg[slots] = X
+    xg = np.zeros((S, fw.n_slots), dtype=np.complex128)
+    xg[:, slots] = X.T
     mass = fw.edge_mass(sigma)
     y = fw.apply(mass, shifts, torch.from_numpy(xg).cuda()).cpu().numpy()
     mask = np.ones(fw.n_slots, bool)
     mask[slots] = False
-    assert np.all(y[mask] == 0)
+    assert np.all(y[:, mask] == 0)
     for s in range(S):
         ref = asm.K @ X[:, s] + shifts[s] * asm.Mdiag * X[:, s]
         scale = np.abs(asm.K) @ np.abs(X[:, s]) + abs(shifts[s]) * asm.Mdiag * np.abs(X[:, s])
-        assert np.all(np.abs(y[slots, s] - ref) <= 1e-13 * scale + 1e-300)
+        assert np.all(np.abs(y[s, slots] - ref) <= 1e-13 * scale + 1e-300)
 
 
 def _term_scale(X, table):
@@ -117,7 +117,7 @@ def test_forward_parity_vs_exact_lu(name):
     Xo = ofw.shifted_solves(asm, table.shifts)
     Uo = ofw.synthesize(Xo, table.residues, table.is_pair)
     ug = u.cpu().numpy()[:, slots].T                      # (N, K)
-    xg = x.cpu().numpy()[slots]
+    xg = x.cpu().numpy()[:, slots].T
     for i, s in enumerate(table.shifts):
         assert ofw.relative_residual(asm, s, xg[:, i]) <= 2e-13
     earth = ~_air_edges(asm, wl)
@@ -142,7 +142,7 @@ def test_cocg_default_tolerance(name):
     mass = fw.edge_mass(sigma)
     x, iters, relres = fw.cocg(mass, f, table.shifts, tol=1e-10, maxit=50000)
     assert np.all(relres <= 1e-10) and np.all(iters > 0)
-    xg = x.cpu().numpy()[slots]
+    xg = x.cpu().numpy()[:, slots].T
     for i, s in enumerate(table.shifts):
         assert ofw.relative_residual(asm, s, xg[:, i]) <= 2e-10
     if asm.n < 20000:
@@ -158,8 +158,8 @@ def test_synthesis_exact():
     rng = np.random.default_rng(0)
     S = table.n_shift
     X = rng.normal(size=(asm.n, S)) + 1j * rng.normal(size=(asm.n, S))
-    xg = np.zeros((fw.n_slots, S), dtype=np.complex128)
-    xg[slots] = X
+    xg = np.zeros((S, fw.n_slots), dtype=np.complex128)
+    xg[:, slots] = X.T
     u = fw.synthesize(torch.from_numpy(xg).cuda(), table.residues, table.is_pair).cpu().numpy()
     Uo = ofw.synthesize(X, table.residues, table.is_pair)
     T = _term_scale(X, table)
@@ -186,7 +186,7 @@ def test_edge_cases():
     # single shift equals the corresponding column of the batched solve
     xb, _, _ = fw.cocg(mass, f, table.shifts, tol=1e-12)
     x1, _, _ = fw.cocg(mass, f, table.shifts[2:3], tol=1e-12)
-    d = (xb[:, 2] - x1[:, 0]).abs().max().item() / xb[:, 2].abs().max().item()
+    d = (xb[2] - x1[0]).abs().max().item() / xb[2].abs().max().item()
     assert d < 1e-6
 
 
