@@ -5,6 +5,7 @@
 produces paper_2506_11657_b200/libtem_b200.so from csrc/*.cu with
 ``nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo``.
 """
+import glob
 import os
 import shutil
 import subprocess
@@ -13,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", "tem_b200.cu")]
-DEPS = SRC + [os.path.join(HERE, "csrc", "tem_device.cuh"), os.path.join(ROOT, "include", "tem_b200.h")]
+DEPS = sorted(glob.glob(os.path.join(HERE, "csrc", "*"))) + [os.path.join(ROOT, "include", "tem_b200.h")]
 LIB = os.path.join(HERE, "libtem_b200.so")
 
 

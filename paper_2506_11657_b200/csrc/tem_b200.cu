@@ -23,6 +23,8 @@
 // device memory; no host round trip per iteration.  The iteration loop is
 // a CUDA graph of `kChunk` iterations; the host checks the active-shift
 // count once per chunk.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -248,11 +250,11 @@ static void sweep_geometry(const tem_ctx* c, int S, tem::SweepArgs& A, int* grid
   A.ntx = (c->g.n[0] + tem::TX - 1) / tem::TX;
   A.nty = (c->g.n[1] + tem::TY - 1) / tem::TY;
   // split z so that the grid covers the machine several times over
-  const int per_wave = c->num_sms * 3;
+  const int per_wave = c->num_sms * 2;
   const int base = A.ntx * A.nty * S;
   int nzc = 1;
   while (base * nzc < 4 * per_wave && c->g.n[2] / (nzc * 2) >= 16) nzc *= 2;
-  A.nzc = nzc;
+  if (const char* env = getenv("TEM_FORCE_NZC")) nzc = std::max(1, atoi(env));  // tests
   A.kchunk = (c->g.n[2] + nzc - 1) / nzc;
   A.nzc = (c->g.n[2] + A.kchunk - 1) / A.kchunk;
   *grid = A.ntx * A.nty * A.nzc * S;
@@ -261,10 +263,34 @@ static void sweep_geometry(const tem_ctx* c, int S, tem::SweepArgs& A, int* grid
 static int sweep_attrs() {
   static bool done = false;
   if (done) return TEM_OK;
-  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSweepSmem));
-  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSweepSmem));
-  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSweepSmem));
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep_direct<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmem2));
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep_direct<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmem2));
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep_dirap, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmem1));
   done = true;
+  return TEM_OK;
+}
+
+// 5-D tiled tensor map over a shift block [S][3][nz+1][ny+1][nx+1] complex
+// fp64 (as 2(nx+1) doubles innermost); box = one halo-extended plane tile.
+static int make_tmap(const tem_ctx* c, int S, const void* base, CUtensorMap* tm) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    TEM_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess)
+      return fail(TEM_ECUDA, "cuTensorMapEncodeTiled not available");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t nx1 = c->g.n[0] + 1, ny1 = c->g.n[1] + 1, nz1 = c->g.n[2] + 1;
+  const cuuint64_t dims[5] = {2 * nx1, ny1, nz1, 3, (cuuint64_t)S};
+  const cuuint64_t strides[4] = {16 * nx1, 16 * nx1 * ny1, 16 * nx1 * ny1 * nz1, 48 * nx1 * ny1 * nz1};
+  const cuuint32_t box[5] = {2 * tem::HX, tem::HY, 1, 1, 1};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<void*>(base), dims, strides,
+                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TEM_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return TEM_OK;
 }
 
@@ -371,10 +397,11 @@ int tem_apply_shifted(tem_ctx* c, const double* mass, int S, const double* shift
   sweep_geometry(c, S, A, &grid);
   for (int s = 0; s < S; ++s) A.shifts[s] = make_double2(shifts[2 * s], shifts[2 * s + 1]);
   A.mass = mass;
-  A.v = reinterpret_cast<const double2*>(x);
   A.out = reinterpret_cast<double2*>(y);
+  CUtensorMap tm;
+  if (int rc = make_tmap(c, S, x, &tm)) return rc;
   TEM_CUDA(cudaMemsetAsync(y, 0, (size_t)3 * c->g.Nn * S * sizeof(double2), (cudaStream_t)stream));
-  tem::k_sweep<0><<<grid, tem::NT, tem::kSweepSmem, (cudaStream_t)stream>>>(A);
+  tem::k_sweep_direct<0><<<grid, tem::NT, tem::kSmem2, (cudaStream_t)stream>>>(A, tm);
   TEM_CUDA(cudaGetLastError());
   return TEM_OK;
 }
@@ -408,8 +435,7 @@ size_t tem_cocg_workspace_bytes(const tem_ctx* c, int S) {
 }
 
 static bool same_args(const tem::SweepArgs& a, const tem::SweepArgs& b) {
-  return a.S == b.S && a.mass == b.mass && a.v == b.v && a.zin == b.zin && a.out == b.out &&
-         a.x == b.x && a.z == b.z && a.st == b.st && a.ctl == b.ctl && a.part_c == b.part_c &&
+  return a.S == b.S && a.mass == b.mass && a.out == b.out && a.x == b.x && a.z == b.z && a.st == b.st && a.ctl == b.ctl && a.part_c == b.part_c &&
          a.part_r == b.part_r && a.g.Nn == b.g.Nn && a.g.ih[0] == b.g.ih[0] && a.nzc == b.nzc;
 }
 
@@ -437,14 +463,14 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
   double2* P[2] = {reinterpret_cast<double2*>(w + L.p0), reinterpret_cast<double2*>(w + L.p1)};
   // iteration parity q: sweep 1 reads p_old = P[q], writes p_new = P[1-q]; sweep 2 reads P[1-q]
   tem::SweepArgs a1[2], a2[2];
+  CUtensorMap tmP[2], tmZ;
   for (int q = 0; q < 2; ++q) {
     a1[q] = base;
-    a1[q].v = P[q];
-    a1[q].zin = base.z;
     a1[q].out = P[1 - q];
     a2[q] = base;
-    a2[q].v = P[1 - q];
+    if (int rc = make_tmap(c, S, P[q], &tmP[q])) return rc;
   }
+  if (int rc = make_tmap(c, S, base.z, &tmZ)) return rc;
 
   // per-shift state + control (host -> device, small)
   std::vector<tem::ShiftState> st(S);
@@ -475,8 +501,9 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
     cudaGraph_t gr;
     TEM_CUDA(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
     for (int it = 0; it < kChunk; ++it) {
-      tem::k_sweep<1><<<grid, tem::NT, tem::kSweepSmem, c->cap_stream>>>(a1[it & 1]);
-      tem::k_sweep<2><<<grid, tem::NT, tem::kSweepSmem, c->cap_stream>>>(a2[it & 1]);
+      const int q = it & 1;
+      tem::k_sweep_dirap<<<grid, tem::NT, tem::kSmem1, c->cap_stream>>>(a1[q], tmZ, tmP[q]);
+      tem::k_sweep_direct<2><<<grid, tem::NT, tem::kSmem2, c->cap_stream>>>(a2[q], tmP[1 - q]);
     }
     TEM_CUDA(cudaStreamEndCapture(c->cap_stream, &gr));
     cudaError_t e = cudaGraphInstantiate(&c->graph, gr, 0);
@@ -493,8 +520,9 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
       TEM_CUDA(cudaGraphLaunch(c->graph, stream));
     } else {
       for (int it = 0; it < chunk; ++it) {
-        tem::k_sweep<1><<<grid, tem::NT, tem::kSweepSmem, stream>>>(a1[(done + it) & 1]);
-        tem::k_sweep<2><<<grid, tem::NT, tem::kSweepSmem, stream>>>(a2[(done + it) & 1]);
+        const int q = (done + it) & 1;
+        tem::k_sweep_dirap<<<grid, tem::NT, tem::kSmem1, stream>>>(a1[q], tmZ, tmP[q]);
+        tem::k_sweep_direct<2><<<grid, tem::NT, tem::kSmem2, stream>>>(a2[q], tmP[1 - q]);
       }
       TEM_CUDA(cudaGetLastError());
     }

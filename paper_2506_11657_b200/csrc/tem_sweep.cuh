@@ -1,25 +1,29 @@
-// tem_sweep.cuh -- the 2.5D z-marching curl-curl sweep (sm_100a).
+// tem_sweep.cuh -- the 2.5D z-marching curl-curl sweep, TMA-fed (sm_100a).
 //
 // One CTA owns a TX x TY tile of nodes in the x-y plane, ONE shift s and a
 // range of node planes k; it marches upward in k.  The halo-extended plane
-// tiles of the swept vector v (x,y components on planes k-1, k, k+1 and the
-// z component on layers k-1, k) live in a shared-memory ring, so every
-// element is fetched from L2/HBM once per sweep (plus the 1-node halo) and
-// the 13-point gather of
+// tiles of the swept vector (x,y components on planes k-1, k, k+1 and the z
+// component on layers k-1, k) live in a shared-memory ring filled by TMA
+// (cp.async.bulk.tensor, 5-D tensor map over the shift-major vector
+// [S][3][nz+1][ny+1][2(nx+1)] fp64; out-of-range halo boxes are zero-filled by
+// the TMA unit, which is exactly the Dirichlet boundary n x e = 0 of eq:bc).
+// Loads run ahead of the arithmetic through a multi-stage mbarrier pipeline,
+// so HBM latency is hidden without per-thread address arithmetic; the
+// 13-point gather of
 //   (K v)_a(m) = W_d(m) C_d(m) - W_d(m-e_b) C_d(m-e_b) - W_b(m) C_b(m) + W_b(m-e_d) C_b(m-e_d)
 // (tem_device.cuh; §2.2, reading R1) reads shared memory only.
-// The next plane set is loaded into registers one step ahead (software
-// pipelining) so its HBM latency overlaps the current step's arithmetic.
 //
 // MODE 0  apply : y = (K + s M) v                                  (tem_apply_shifted)
-// MODE 1  dirap : v = p_new = z + beta p_old formed on load; writes p_new;
-//                 mu = p_new^T (K + s M) p_new                      (COCG sweep 1)
+// MODE 1  dirap : p_new = z + beta p_old formed from TMA-staged z and p_old
+//                 tiles; writes p_new; mu = p_new^T (K + s M) p_new (COCG sweep 1)
 // MODE 2  upd   : v = p; x += alpha p; z -= alpha D^-1 (K + s M) p;
 //                 rho = (D z)^T z, ||D z||^2                        (COCG sweep 2)
 // z = D^-1 r is stored instead of r (reading "z-form"): r = D z
 // is recovered where needed, so a COCG iteration streams x, z, p_old, p_new
 // at the 128 B / unknown / shift minimum of a two-reduction COCG.
 #pragma once
+#include <cuda.h>
+
 #include "tem_device.cuh"
 
 namespace tem {
@@ -28,9 +32,16 @@ constexpr int TX = 32;                    // tile nodes along x (one warp row)
 constexpr int TY = 8;                     // tile nodes along y
 constexpr int NT = TX * TY;               // threads per CTA
 constexpr int HX = TX + 2, HY = TY + 2;   // halo-extended tile
-constexpr int H = HX * HY;                // nodes per plane tile
-constexpr int LOADS = (3 * H + NT - 1) / NT;  // plane-set elements per thread per step
-constexpr size_t kSweepSmem = (size_t)11 * H * sizeof(double2);  // dynamic shared memory
+constexpr int TILE_BYTES = HX * HY * 16;  // one plane tile as delivered by TMA (5440 B)
+constexpr int TILE_STRIDE = (TILE_BYTES + 127) / 128 * 128;   // slot pitch (128 B aligned)
+constexpr int TS2 = TILE_STRIDE / 16;     // slot pitch in double2
+
+// MODE 0/2 ring (direct): sets q = {X(q+1), Y(q+1), Z(q)}; X,Y: 5 slots, Z: 4 slots
+constexpr int R2_XY = 5, R2_Z = 4;
+constexpr size_t kSmem2 = 128 + (size_t)(2 * R2_XY + R2_Z) * TILE_STRIDE;
+// MODE 1: p_new ring X,Y: 4 slots, Z: 3 slots; raw staging: 2 slots x 6 tiles (z, p_old)
+constexpr int R1_XY = 4, R1_Z = 3, R1_ST = 2;
+constexpr size_t kSmem1 = 128 + (size_t)(2 * R1_XY + R1_Z + 6 * R1_ST) * TILE_STRIDE;
 
 struct ShiftState {
   double2 s;        // shift
@@ -56,8 +67,6 @@ struct SweepArgs {
   int S;
   int ntx, nty, nzc, kchunk;   // tiles along x, y; z-chunks and their length
   const double* mass;          // [3][Nn]
-  const double2* v;            // swept vector [S][3][Nn] (MODE 0: x; MODE 1: p_old; MODE 2: p)
-  const double2* zin;          // MODE 1: z
   double2* out;                // MODE 0: y; MODE 1: p_new
   double2* x;                  // MODE 2
   double2* z;                  // MODE 2 (in/out)
@@ -67,6 +76,45 @@ struct SweepArgs {
   double* part_r;              // [gridDim]
   double2 shifts[32];          // MODE 0 only
 };
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// 5-D tiled TMA load of one plane tile: coords (2(i0-1), j0-1, k, comp, shift)
+__device__ __forceinline__ void tma_tile(void* dst, const CUtensorMap* tm, int c0, int c1, int c2,
+                                         int c3, int c4, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ int pmod(int q, int n) { return ((q % n) + n) % n; }
 
 __device__ __forceinline__ bool free_x(const Grid& g, int i, int j, int k) {
   return i < g.n[0] && j >= 1 && j <= g.n[1] - 1 && k >= 1 && k <= g.n[2] - 1;
@@ -123,206 +171,103 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(NT, 3) k_sweep(SweepArgs A) {
-  // ring: X, Y planes (4 slots each: k-1, k, k+1 and the one being filled), Z layers (3 slots)
-  extern __shared__ double2 smem_ring[];
-  double2 (*sX)[H] = reinterpret_cast<double2 (*)[H]>(smem_ring);
-  double2 (*sY)[H] = reinterpret_cast<double2 (*)[H]>(smem_ring + 4 * H);
-  double2 (*sZ)[H] = reinterpret_cast<double2 (*)[H]>(smem_ring + 8 * H);
-  __shared__ double red[3 * NT / 32];
+// Column constants of thread (i, j) of the tile.
+struct Column {
+  int i, j, c0;
+  bool in_ij;
+  double ihx, ihxm, ihy, ihym, hdx, hdy;
+};
 
-  const Grid& g = A.g;
-  const int S = A.S;
-  // block -> (z-chunk, xy tile, shift), shift fastest so that the S CTAs of a
-  // tile run together and share its coefficients through L2
-  const int s = blockIdx.x % S;
-  const int xy = (blockIdx.x / S) % (A.ntx * A.nty);
-  const int zc = blockIdx.x / (S * A.ntx * A.nty);
-  const int tx0 = (xy % A.ntx) * TX, ty0 = (xy / A.ntx) * TY;
-  const int kb = zc * A.kchunk;
-  const int ke = min(kb + A.kchunk, g.n[2]);
-
-  double2 sh, beta, alpha;
-  bool live;
-  if (MODE == 0) {
-    sh = A.shifts[s];
-    live = true;
-  } else {
-    const ShiftState& st = A.st[s];
-    sh = st.s;
-    beta = st.beta;
-    alpha = st.alpha;
-    live = st.active != 0;
-  }
-
-  double2 acc_c = czero();
-  double acc_r = 0.0;
-  const int nx1 = g.n[0] + 1, ny1 = g.n[1] + 1, nz = g.n[2];
-  const long long vs = (long long)s * 3 * g.Nn;   // shift offset
+__device__ __forceinline__ Column make_column(const Grid& g, int tx0, int ty0) {
+  Column C;
   const int tid = threadIdx.x;
+  C.i = tx0 + (tid % TX);
+  C.j = ty0 + (tid / TX);
+  C.c0 = ((tid / TX) + 1) * HX + (tid % TX) + 1;
+  C.in_ij = C.i < g.n[0] && C.j < g.n[1];
+  C.ihx = C.in_ij ? __ldg(g.ih[0] + C.i) : 0.0;
+  C.ihxm = (C.in_ij && C.i >= 1) ? __ldg(g.ih[0] + C.i - 1) : 0.0;
+  C.ihy = C.in_ij ? __ldg(g.ih[1] + C.j) : 0.0;
+  C.ihym = (C.in_ij && C.j >= 1) ? __ldg(g.ih[1] + C.j - 1) : 0.0;
+  C.hdx = C.in_ij ? __ldg(g.hdm[0] + C.i) : 0.0;
+  C.hdy = C.in_ij ? __ldg(g.hdm[1] + C.j) : 0.0;
+  return C;
+}
 
-  if (live) {
-    // per-thread constants of the column (i, j)
-    const int i = tx0 + (tid % TX), j = ty0 + (tid / TX);
-    const int li = (tid % TX) + 1, lj = (tid / TX) + 1;
-    const int c0 = lj * HX + li;          // centre in a plane tile
-    const bool in_ij = i < g.n[0] && j < g.n[1];
-    const double ihx = in_ij ? __ldg(g.ih[0] + i) : 0.0;
-    const double ihxm = (in_ij && i >= 1) ? __ldg(g.ih[0] + i - 1) : 0.0;
-    const double ihy = in_ij ? __ldg(g.ih[1] + j) : 0.0;
-    const double ihym = (in_ij && j >= 1) ? __ldg(g.ih[1] + j - 1) : 0.0;
-    const double hdx = in_ij ? __ldg(g.hdm[0] + i) : 0.0;
-    const double hdy = in_ij ? __ldg(g.hdm[1] + j) : 0.0;
+// K v for the three edges of node (i, j, k) from ring tiles:
+// Xm/X0/Xp = x-comp planes k-1/k/k+1, same for Y; Zm/Z0 = z-comp layers k-1/k.
+struct Edge3 {
+  double2 q[3], p[3];
+  double kd[3];
+  bool f[3];
+};
 
-    // plane-set loader: element e of {X(kx), Y(kx), Z(kz)} tiles
-    auto load_elem = [&](int e, int kx, int kz, const double2* __restrict__ src) -> double2 {
-      const int comp = e / H;
-      const int r = e - comp * H;
-      const int ii = tx0 - 1 + (r % HX), jj = ty0 - 1 + (r / HX);
-      const int kk = comp == 2 ? kz : kx;
-      if (ii < 0 || ii >= nx1 || jj < 0 || jj >= ny1 || kk < 0 || kk > nz) return czero();
-      return __ldg(src + vs + (long long)comp * g.Nn + ((long long)kk * ny1 + jj) * nx1 + ii);
-    };
-    auto store_elem = [&](int e, int slot_xy, int slot_z, double2 v) {
-      const int comp = e / H;
-      const int r = e - comp * H;
-      if (comp == 0) sX[slot_xy][r] = v;
-      else if (comp == 1) sY[slot_xy][r] = v;
-      else sZ[slot_z][r] = v;
-    };
-    auto fetch = [&](int e, int kx, int kz) -> double2 {
-      // MODE 1 forms p_new = z + beta p_old on load
-      if (MODE == 1) {
-        const double2 zv = load_elem(e, kx, kz, A.zin);
-        const double2 pv = load_elem(e, kx, kz, A.v);
-        return cfma(beta, pv, zv);
-      }
-      return load_elem(e, kx, kz, A.v);
-    };
-
-    // prologue: X,Y planes kb-1, kb ; Z layer kb-1 ; then X,Y kb+1 and Z kb
-    for (int e = tid; e < 3 * H; e += NT) store_elem(e, (kb + 3) & 3, (kb + 2) % 3, fetch(e, kb - 1, kb - 1));
-    for (int e = tid; e < 2 * H; e += NT) store_elem(e, kb & 3, 0, fetch(e, kb, kb));
-    for (int e = tid; e < 3 * H; e += NT) store_elem(e, (kb + 1) & 3, kb % 3, fetch(e, kb + 1, kb));
-    __syncthreads();
-
-    for (int k = kb; k < ke; ++k) {
-      // 1. issue the loads of the next plane set (X,Y plane k+2, Z layer k+1)
-      double2 nxt[LOADS];
+__device__ __forceinline__ void stencil3(const Grid& g, const Column& C, int k, const double2* Xm,
+                                         const double2* X0, const double2* Xp, const double2* Ym,
+                                         const double2* Y0, const double2* Yp, const double2* Zm,
+                                         const double2* Z0, Edge3& E) {
+  const double ihz = __ldg(g.ih[2] + k);
+  const double ihzm = k >= 1 ? __ldg(g.ih[2] + k - 1) : 0.0;
+  const double hdz = __ldg(g.hdm[2] + k);
+  const int c0 = C.c0;
+  E.f[0] = C.in_ij && free_x(g, C.i, C.j, k);
+  E.f[1] = C.in_ij && free_y(g, C.i, C.j, k);
+  E.f[2] = C.in_ij && free_z(g, C.i, C.j, k);
+#define T_(P, di, dj) P[c0 + (dj) * HX + (di)]
 #pragma unroll
-      for (int q = 0; q < LOADS; ++q) {
-        const int e = tid + q * NT;
-        nxt[q] = e < 3 * H ? fetch(e, k + 2, k + 1) : czero();
-      }
-      // 2. compute the three edges of node (i, j, k) from shared memory
-      const int xm = (k + 3) & 3, x0 = k & 3, xp = (k + 1) & 3;
-      const int zm = (k + 2) % 3, z0 = k % 3;
-      const double ihz = __ldg(g.ih[2] + k);
-      const double ihzm = k >= 1 ? __ldg(g.ih[2] + k - 1) : 0.0;
-      const double hdz = __ldg(g.hdm[2] + k);
-      const long long node = ((long long)k * ny1 + j) * nx1 + i;
-#define X_(dk, di, dj) sX[dk][c0 + (dj) * HX + (di)]
-#define Y_(dk, di, dj) sY[dk][c0 + (dj) * HX + (di)]
-#define Z_(dk, di, dj) sZ[dk][c0 + (dj) * HX + (di)]
-      double2 q3[3], p3[3];
-      double m3[3], kd3[3];
-      bool f3[3];
-      f3[0] = in_ij && free_x(g, i, j, k);
-      f3[1] = in_ij && free_y(g, i, j, k);
-      f3[2] = in_ij && free_z(g, i, j, k);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        q3[c] = czero();
-        p3[c] = czero();
-        m3[c] = 0.0;
-        kd3[c] = 0.0;
-      }
-      if (f3[0]) {  // x-edge: A=x, B=y, D=z
-        const double2 a0 = X_(x0, 0, 0);
-        const double2 cD0 = csub(cadd(a0, Y_(x0, 1, 0)), cadd(X_(x0, 0, 1), Y_(x0, 0, 0)));
-        const double2 cD1 = csub(cadd(X_(x0, 0, -1), Y_(x0, 1, -1)), cadd(a0, Y_(x0, 0, -1)));
-        const double2 cB0 = csub(cadd(Z_(z0, 0, 0), X_(xp, 0, 0)), cadd(Z_(z0, 1, 0), a0));
-        const double2 cB1 = csub(cadd(Z_(zm, 0, 0), a0), cadd(Z_(zm, 1, 0), X_(xm, 0, 0)));
-        const double wD0 = hdz * ihx * ihy, wD1 = hdz * ihx * ihym;
-        const double wB0 = hdy * ihx * ihz, wB1 = hdy * ihx * ihzm;
-        q3[0] = make_double2(wD0 * cD0.x - wD1 * cD1.x - wB0 * cB0.x + wB1 * cB1.x,
-                             wD0 * cD0.y - wD1 * cD1.y - wB0 * cB0.y + wB1 * cB1.y);
-        kd3[0] = wD0 + wD1 + wB0 + wB1;
-        p3[0] = a0;
-      }
-      if (f3[1]) {  // y-edge: A=y, B=z, D=x
-        const double2 a0 = Y_(x0, 0, 0);
-        const double2 cD0 = csub(cadd(a0, Z_(z0, 0, 1)), cadd(Y_(xp, 0, 0), Z_(z0, 0, 0)));
-        const double2 cD1 = csub(cadd(Y_(xm, 0, 0), Z_(zm, 0, 1)), cadd(a0, Z_(zm, 0, 0)));
-        const double2 cB0 = csub(cadd(X_(x0, 0, 0), Y_(x0, 1, 0)), cadd(X_(x0, 0, 1), a0));
-        const double2 cB1 = csub(cadd(X_(x0, -1, 0), a0), cadd(X_(x0, -1, 1), Y_(x0, -1, 0)));
-        const double wD0 = hdx * ihy * ihz, wD1 = hdx * ihy * ihzm;
-        const double wB0 = hdz * ihy * ihx, wB1 = hdz * ihy * ihxm;
-        q3[1] = make_double2(wD0 * cD0.x - wD1 * cD1.x - wB0 * cB0.x + wB1 * cB1.x,
-                             wD0 * cD0.y - wD1 * cD1.y - wB0 * cB0.y + wB1 * cB1.y);
-        kd3[1] = wD0 + wD1 + wB0 + wB1;
-        p3[1] = a0;
-      }
-      if (f3[2]) {  // z-edge: A=z, B=x, D=y
-        const double2 a0 = Z_(z0, 0, 0);
-        const double2 cD0 = csub(cadd(a0, X_(xp, 0, 0)), cadd(Z_(z0, 1, 0), X_(x0, 0, 0)));
-        const double2 cD1 = csub(cadd(Z_(z0, -1, 0), X_(xp, -1, 0)), cadd(a0, X_(x0, -1, 0)));
-        const double2 cB0 = csub(cadd(Y_(x0, 0, 0), Z_(z0, 0, 1)), cadd(Y_(xp, 0, 0), a0));
-        const double2 cB1 = csub(cadd(Y_(x0, 0, -1), a0), cadd(Y_(xp, 0, -1), Z_(z0, 0, -1)));
-        const double wD0 = hdy * ihz * ihx, wD1 = hdy * ihz * ihxm;
-        const double wB0 = hdx * ihz * ihy, wB1 = hdx * ihz * ihym;
-        q3[2] = make_double2(wD0 * cD0.x - wD1 * cD1.x - wB0 * cB0.x + wB1 * cB1.x,
-                             wD0 * cD0.y - wD1 * cD1.y - wB0 * cB0.y + wB1 * cB1.y);
-        kd3[2] = wD0 + wD1 + wB0 + wB1;
-        p3[2] = a0;
-      }
-#undef X_
-#undef Y_
-#undef Z_
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        if (!f3[c]) continue;
-        const long long slot = (long long)c * g.Nn + node;
-        const double m = __ldg(A.mass + slot);
-        const double2 q = cfma(sh, cscale(m, p3[c]), q3[c]);   // (K + s M) v
-        if (MODE == 0) {
-          A.out[vs + slot] = q;
-        } else if (MODE == 1) {
-          A.out[vs + slot] = p3[c];                          // p_new
-          acc_c = cfma(p3[c], q, acc_c);                     // p^T A p
-        } else {
-          const double2 D = make_double2(kd3[c] + m * sh.x, m * sh.y);
-          const long long e = vs + slot;
-          A.x[e] = cfma(alpha, p3[c], A.x[e]);
-          // z_new = z - alpha D^-1 q ; r_new = D z_new
-          const double2 zn = csub(A.z[e], cmul(alpha, cdiv(q, D)));
-          A.z[e] = zn;
-          const double2 rn = cmul(D, zn);
-          acc_c = cfma(rn, zn, acc_c);                       // r^T z
-          acc_r += rn.x * rn.x + rn.y * rn.y;                // ||r||^2
-        }
-      }
-      // 3. commit the prefetched plane set into the free ring slots
-      const int wx = (k + 2) & 3, wz = (k + 1) % 3;
-#pragma unroll
-      for (int q = 0; q < LOADS; ++q) {
-        const int e = tid + q * NT;
-        if (e < 3 * H) store_elem(e, wx, wz, nxt[q]);
-      }
-      __syncthreads();
-    }
+  for (int c = 0; c < 3; ++c) {
+    E.q[c] = czero();
+    E.p[c] = czero();
+    E.kd[c] = 0.0;
   }
-
-  if (MODE == 0) return;
-  // ---- per-CTA partial -> last CTA finalises the per-shift scalars
-  block_sum_n<NT>(acc_c, acc_r, red);
-  if (tid == 0) {
-    A.part_c[blockIdx.x] = acc_c;
-    A.part_r[blockIdx.x] = acc_r;
+  if (E.f[0]) {  // x-edge: A=x, B=y, D=z
+    const double2 a0 = T_(X0, 0, 0);
+    const double2 cD0 = csub(cadd(a0, T_(Y0, 1, 0)), cadd(T_(X0, 0, 1), T_(Y0, 0, 0)));
+    const double2 cD1 = csub(cadd(T_(X0, 0, -1), T_(Y0, 1, -1)), cadd(a0, T_(Y0, 0, -1)));
+    const double2 cB0 = csub(cadd(T_(Z0, 0, 0), T_(Xp, 0, 0)), cadd(T_(Z0, 1, 0), a0));
+    const double2 cB1 = csub(cadd(T_(Zm, 0, 0), a0), cadd(T_(Zm, 1, 0), T_(Xm, 0, 0)));
+    const double wD0 = hdz * C.ihx * C.ihy, wD1 = hdz * C.ihx * C.ihym;
+    const double wB0 = C.hdy * C.ihx * ihz, wB1 = C.hdy * C.ihx * ihzm;
+    E.q[0] = make_double2(wD0 * cD0.x - wD1 * cD1.x - wB0 * cB0.x + wB1 * cB1.x,
+                          wD0 * cD0.y - wD1 * cD1.y - wB0 * cB0.y + wB1 * cB1.y);
+    E.kd[0] = wD0 + wD1 + wB0 + wB1;
+    E.p[0] = a0;
   }
-  if (!last_block(&A.ctl->ticket[MODE])) return;
-  const int warp = tid >> 5, lane = tid & 31;
+  if (E.f[1]) {  // y-edge: A=y, B=z, D=x
+    const double2 a0 = T_(Y0, 0, 0);
+    const double2 cD0 = csub(cadd(a0, T_(Z0, 0, 1)), cadd(T_(Yp, 0, 0), T_(Z0, 0, 0)));
+    const double2 cD1 = csub(cadd(T_(Ym, 0, 0), T_(Zm, 0, 1)), cadd(a0, T_(Zm, 0, 0)));
+    const double2 cB0 = csub(cadd(T_(X0, 0, 0), T_(Y0, 1, 0)), cadd(T_(X0, 0, 1), a0));
+    const double2 cB1 = csub(cadd(T_(X0, -1, 0), a0), cadd(T_(X0, -1, 1), T_(Y0, -1, 0)));
+    const double wD0 = C.hdx * C.ihy * ihz, wD1 = C.hdx * C.ihy * ihzm;
+    const double wB0 = hdz * C.ihy * C.ihx, wB1 = hdz * C.ihy * C.ihxm;
+    E.q[1] = make_double2(wD0 * cD0.x - wD1 * cD1.x - wB0 * cB0.x + wB1 * cB1.x,
+                          wD0 * cD0.y - wD1 * cD1.y - wB0 * cB0.y + wB1 * cB1.y);
+    E.kd[1] = wD0 + wD1 + wB0 + wB1;
+    E.p[1] = a0;
+  }
+  if (E.f[2]) {  // z-edge: A=z, B=x, D=y
+    const double2 a0 = T_(Z0, 0, 0);
+    const double2 cD0 = csub(cadd(a0, T_(Xp, 0, 0)), cadd(T_(Z0, 1, 0), T_(X0, 0, 0)));
+    const double2 cD1 = csub(cadd(T_(Z0, -1, 0), T_(Xp, -1, 0)), cadd(a0, T_(X0, -1, 0)));
+    const double2 cB0 = csub(cadd(T_(Y0, 0, 0), T_(Z0, 0, 1)), cadd(T_(Yp, 0, 0), a0));
+    const double2 cB1 = csub(cadd(T_(Y0, 0, -1), a0), cadd(T_(Yp, 0, -1), T_(Z0, 0, -1)));
+    const double wD0 = C.hdy * ihz * C.ihx, wD1 = C.hdy * ihz * C.ihxm;
+    const double wB0 = C.hdx * ihz * C.ihy, wB1 = C.hdx * ihz * C.ihym;
+    E.q[2] = make_double2(wD0 * cD0.x - wD1 * cD1.x - wB0 * cB0.x + wB1 * cB1.x,
+                          wD0 * cD0.y - wD1 * cD1.y - wB0 * cB0.y + wB1 * cB1.y);
+    E.kd[2] = wD0 + wD1 + wB0 + wB1;
+    E.p[2] = a0;
+  }
+#undef T_
+}
+
+// Finalisation by the last CTA: per-shift sums of the per-CTA partials
+// (CTAs of shift q are blockIdx = q mod S), scalar updates of COCG.
+template <int MODE>
+__device__ void finalize(const SweepArgs& A) {
+  const int S = A.S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nblk = gridDim.x;
   for (int q = warp; q < S; q += NT / 32) {
     ShiftState& sq = A.st[q];
@@ -364,12 +309,284 @@ __global__ void __launch_bounds__(NT, 3) k_sweep(SweepArgs A) {
     }
   }
   __syncthreads();
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     int na = 0;
     for (int q = 0; q < S; ++q) na += A.st[q].active;
     A.ctl->n_active = na;
     A.ctl->ticket[MODE] = 0;
   }
+}
+
+__device__ __forceinline__ void block_coords(const SweepArgs& A, int& s, int& tx0, int& ty0, int& kb,
+                                             int& ke) {
+  // block -> (z-chunk, xy tile, shift), shift fastest so that the S CTAs of a
+  // tile run together and share its coefficients through L2
+  const int S = A.S;
+  s = blockIdx.x % S;
+  const int xy = (blockIdx.x / S) % (A.ntx * A.nty);
+  const int zc = blockIdx.x / (S * A.ntx * A.nty);
+  tx0 = (xy % A.ntx) * TX;
+  ty0 = (xy / A.ntx) * TY;
+  kb = zc * A.kchunk;
+  ke = min(kb + A.kchunk, A.g.n[2]);
+}
+
+// ---------------------------------------------------------------- MODE 0, 2
+template <int MODE>
+__global__ void __launch_bounds__(NT, 2) k_sweep_direct(const __grid_constant__ SweepArgs A,
+                                                        const __grid_constant__ CUtensorMap tmv) {
+  extern __shared__ unsigned char smem_raw[];
+  double2* ring = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  double2* rX = ring;                        // [R2_XY] slots
+  double2* rY = ring + R2_XY * TS2;          // [R2_XY]
+  double2* rZ = ring + 2 * R2_XY * TS2;      // [R2_Z]
+  __shared__ __align__(8) uint64_t bar[R2_XY];
+  __shared__ double red[3 * NT / 32];
+
+  const Grid& g = A.g;
+  int s, tx0, ty0, kb, ke;
+  block_coords(A, s, tx0, ty0, kb, ke);
+  const int tid = threadIdx.x;
+
+  double2 sh, alpha;
+  bool live;
+  if (MODE == 0) {
+    sh = A.shifts[s];
+    alpha = czero();
+    live = true;
+  } else {
+    const ShiftState& st = A.st[s];
+    sh = st.s;
+    alpha = st.alpha;
+    live = st.active != 0;
+  }
+  double2 acc_c = czero();
+  double acc_r = 0.0;
+
+  if (live) {
+    const Column C = make_column(g, tx0, ty0);
+    const long long vs = (long long)s * 3 * g.Nn;
+    const int nx1 = g.n[0] + 1, ny1 = g.n[1] + 1;
+    // set q = {X(q+1), Y(q+1), Z(q)} -> slots q mod 5 (X,Y), q mod 4 (Z); barrier q mod 5.
+    // Set kb-2 carries no Z tile: Z(kb-2) is never read, and with 5 sets in
+    // flight its Z slot is the one set kb+2 fills (two TMAs into one slot race).
+    auto issue = [&](int q) {
+      const int sx = pmod(q, R2_XY), sz = pmod(q, R2_Z);
+      const bool with_z = q > kb - 2;
+      mbar_expect_tx(&bar[sx], (with_z ? 3 : 2) * TILE_BYTES);
+      tma_tile(rX + sx * TS2, &tmv, 2 * (tx0 - 1), ty0 - 1, q + 1, 0, s, &bar[sx]);
+      tma_tile(rY + sx * TS2, &tmv, 2 * (tx0 - 1), ty0 - 1, q + 1, 1, s, &bar[sx]);
+      if (with_z) tma_tile(rZ + sz * TS2, &tmv, 2 * (tx0 - 1), ty0 - 1, q, 2, s, &bar[sx]);
+    };
+    if (tid == 0) {
+      for (int q = 0; q < R2_XY; ++q) mbar_init(&bar[q], 1);
+      fence_barrier_init();
+    }
+    __syncthreads();
+    if (tid == 0)
+      for (int q = kb - 2; q <= min(kb + 2, ke - 1); ++q) issue(q);
+    uint32_t phase = 0;   // bit b = parity of the next wait on bar[b]
+    auto wait_set = [&](int q) {
+      const int b = pmod(q, R2_XY);
+      mbar_wait(&bar[b], (phase >> b) & 1u);
+      phase ^= 1u << b;
+    };
+    wait_set(kb - 2);
+    wait_set(kb - 1);
+
+    // centre operands of step k, loaded one step ahead
+    auto node_of = [&](int k) { return ((long long)k * ny1 + C.j) * nx1 + C.i; };
+    double mN[3];
+    double2 xN[3], zN[3];
+    auto load_centre = [&](int k) {
+      const long long node = node_of(k);
+      const bool ok = C.in_ij && k < g.n[2];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const long long slot = (long long)c * g.Nn + node;
+        mN[c] = ok ? __ldg(A.mass + slot) : 0.0;
+        if (MODE == 2) {
+          xN[c] = ok ? A.x[vs + slot] : czero();
+          zN[c] = ok ? A.z[vs + slot] : czero();
+        }
+      }
+    };
+    load_centre(kb);
+
+    for (int k = kb; k < ke; ++k) {
+      double mC[3];
+      double2 xC[3], zC[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        mC[c] = mN[c];
+        if (MODE == 2) {
+          xC[c] = xN[c];
+          zC[c] = zN[c];
+        }
+      }
+      if (k + 1 < ke) load_centre(k + 1);
+      wait_set(k);
+      Edge3 E;
+      stencil3(g, C, k, rX + pmod(k - 2, R2_XY) * TS2, rX + pmod(k - 1, R2_XY) * TS2,
+               rX + pmod(k, R2_XY) * TS2, rY + pmod(k - 2, R2_XY) * TS2,
+               rY + pmod(k - 1, R2_XY) * TS2, rY + pmod(k, R2_XY) * TS2,
+               rZ + pmod(k - 1, R2_Z) * TS2, rZ + pmod(k, R2_Z) * TS2, E);
+      const long long node = node_of(k);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        if (!E.f[c]) continue;
+        const long long e = vs + (long long)c * g.Nn + node;
+        const double2 q = cfma(sh, cscale(mC[c], E.p[c]), E.q[c]);   // (K + s M) v
+        if (MODE == 0) {
+          A.out[e] = q;
+        } else {
+          const double2 D = make_double2(E.kd[c] + mC[c] * sh.x, mC[c] * sh.y);
+          A.x[e] = cfma(alpha, E.p[c], xC[c]);
+          const double2 zn = csub(zC[c], cmul(alpha, cdiv(q, D)));   // z - alpha D^-1 q
+          A.z[e] = zn;
+          const double2 rn = cmul(D, zn);                           // r = D z
+          acc_c = cfma(rn, zn, acc_c);
+          acc_r += rn.x * rn.x + rn.y * rn.y;
+        }
+      }
+      __syncthreads();   // all reads of set k-2 done -> its slots may be refilled
+      if (tid == 0 && k + 3 <= ke - 1) {
+        fence_proxy_async();
+        issue(k + 3);
+      }
+    }
+  }
+  if (MODE == 0) return;
+  block_sum_n<NT>(acc_c, acc_r, red);
+  if (tid == 0) {
+    A.part_c[blockIdx.x] = acc_c;
+    A.part_r[blockIdx.x] = acc_r;
+  }
+  if (!last_block(&A.ctl->ticket[MODE])) return;
+  finalize<MODE>(A);
+}
+
+// ---------------------------------------------------------------- MODE 1
+__global__ void __launch_bounds__(NT, 2) k_sweep_dirap(const __grid_constant__ SweepArgs A,
+                                                       const __grid_constant__ CUtensorMap tmz,
+                                                       const __grid_constant__ CUtensorMap tmp) {
+  extern __shared__ unsigned char smem_raw[];
+  double2* base = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  double2* rX = base;                              // p_new ring [R1_XY]
+  double2* rY = base + R1_XY * TS2;                // [R1_XY]
+  double2* rZ = base + 2 * R1_XY * TS2;            // [R1_Z]
+  double2* stg = base + (2 * R1_XY + R1_Z) * TS2;  // staging [R1_ST][6 tiles]: zX zY zZ pX pY pZ
+  __shared__ __align__(8) uint64_t bar[R1_ST];
+  __shared__ double red[3 * NT / 32];
+
+  const Grid& g = A.g;
+  int s, tx0, ty0, kb, ke;
+  block_coords(A, s, tx0, ty0, kb, ke);
+  const int tid = threadIdx.x;
+
+  const ShiftState& stt = A.st[s];
+  const double2 sh = stt.s;
+  const double2 beta = stt.beta;
+  const bool live = stt.active != 0;
+  double2 acc_c = czero();
+  double acc_r = 0.0;
+
+  if (live) {
+    const Column C = make_column(g, tx0, ty0);
+    const long long vs = (long long)s * 3 * g.Nn;
+    const int nx1 = g.n[0] + 1, ny1 = g.n[1] + 1;
+    // raw set q = z and p_old tiles {X(q+1), Y(q+1), Z(q)} -> staging slot q mod 2
+    auto issue = [&](int q) {
+      const int b = pmod(q, R1_ST);
+      double2* d = stg + b * 6 * TS2;
+      mbar_expect_tx(&bar[b], 6 * TILE_BYTES);
+      tma_tile(d + 0 * TS2, &tmz, 2 * (tx0 - 1), ty0 - 1, q + 1, 0, s, &bar[b]);
+      tma_tile(d + 1 * TS2, &tmz, 2 * (tx0 - 1), ty0 - 1, q + 1, 1, s, &bar[b]);
+      tma_tile(d + 2 * TS2, &tmz, 2 * (tx0 - 1), ty0 - 1, q, 2, s, &bar[b]);
+      tma_tile(d + 3 * TS2, &tmp, 2 * (tx0 - 1), ty0 - 1, q + 1, 0, s, &bar[b]);
+      tma_tile(d + 4 * TS2, &tmp, 2 * (tx0 - 1), ty0 - 1, q + 1, 1, s, &bar[b]);
+      tma_tile(d + 5 * TS2, &tmp, 2 * (tx0 - 1), ty0 - 1, q, 2, s, &bar[b]);
+    };
+    uint32_t phase = 0;
+    // wait raw set q, combine p_new = z + beta p_old into ring slots q mod 4 / q mod 3
+    auto combine = [&](int q) {
+      const int b = pmod(q, R1_ST);
+      mbar_wait(&bar[b], (phase >> b) & 1u);
+      phase ^= 1u << b;
+      const double2* d = stg + b * 6 * TS2;
+      double2* dX = rX + pmod(q, R1_XY) * TS2;
+      double2* dY = rY + pmod(q, R1_XY) * TS2;
+      double2* dZ = rZ + pmod(q, R1_Z) * TS2;
+      for (int e = tid; e < HX * HY; e += NT) {
+        dX[e] = cfma(beta, d[3 * TS2 + e], d[0 * TS2 + e]);
+        dY[e] = cfma(beta, d[4 * TS2 + e], d[1 * TS2 + e]);
+        dZ[e] = cfma(beta, d[5 * TS2 + e], d[2 * TS2 + e]);
+      }
+    };
+    if (tid == 0) {
+      for (int q = 0; q < R1_ST; ++q) mbar_init(&bar[q], 1);
+      fence_barrier_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+      issue(kb - 2);
+      issue(kb - 1);
+    }
+    // prologue: sets kb-2, kb-1, kb into the ring; raw kb+1, kb+2 left in flight
+    for (int q = kb - 2; q <= kb; ++q) {
+      combine(q);
+      __syncthreads();
+      if (tid == 0 && q + 2 <= ke - 1) {
+        fence_proxy_async();
+        issue(q + 2);
+      }
+    }
+    auto node_of = [&](int k) { return ((long long)k * ny1 + C.j) * nx1 + C.i; };
+    double mN[3];
+    auto load_mass = [&](int k) {
+      const long long node = node_of(k);
+      const bool ok = C.in_ij && k < g.n[2];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) mN[c] = ok ? __ldg(A.mass + (long long)c * g.Nn + node) : 0.0;
+    };
+    load_mass(kb);
+
+    for (int k = kb; k < ke; ++k) {
+      double mC[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) mC[c] = mN[c];
+      if (k + 1 < ke) load_mass(k + 1);
+      Edge3 E;
+      stencil3(g, C, k, rX + pmod(k - 2, R1_XY) * TS2, rX + pmod(k - 1, R1_XY) * TS2,
+               rX + pmod(k, R1_XY) * TS2, rY + pmod(k - 2, R1_XY) * TS2,
+               rY + pmod(k - 1, R1_XY) * TS2, rY + pmod(k, R1_XY) * TS2,
+               rZ + pmod(k - 1, R1_Z) * TS2, rZ + pmod(k, R1_Z) * TS2, E);
+      const long long node = node_of(k);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        if (!E.f[c]) continue;
+        const long long e = vs + (long long)c * g.Nn + node;
+        const double2 q = cfma(sh, cscale(mC[c], E.p[c]), E.q[c]);
+        A.out[e] = E.p[c];                 // p_new
+        acc_c = cfma(E.p[c], q, acc_c);    // p^T A p
+      }
+      // the ring slots of set k+1 held set k-3 (no longer read): combine the
+      // raw set k+1 there, then refill its staging slot with raw set k+3
+      if (k + 1 <= ke - 1) combine(k + 1);
+      __syncthreads();
+      if (tid == 0 && k + 3 <= ke - 1) {
+        fence_proxy_async();
+        issue(k + 3);
+      }
+    }
+  }
+  block_sum_n<NT>(acc_c, acc_r, red);
+  if (tid == 0) {
+    A.part_c[blockIdx.x] = acc_c;
+    A.part_r[blockIdx.x] = acc_r;
+  }
+  if (!last_block(&A.ctl->ticket[1])) return;
+  finalize<1>(A);
 }
 
 }  // namespace tem

@@ -67,9 +67,15 @@ def test_edge_mass(name):
     assert np.all(m[mask] == 0.0)
 
 
+@pytest.mark.parametrize("nzc", ["", "2", "3"])
 @pytest.mark.parametrize("name,S", [("tiny", 8), ("ragged", 10), ("ragged2", 1), ("block", 32),
                                     ("min2", 3)])
-def test_apply_shifted(name, S):
+def test_apply_shifted(name, S, nzc, monkeypatch):
+    """Operator apply vs the oracle CSR, element-wise; also with the z-range
+    of each tile split into 2 / 3 chunks (TEM_FORCE_NZC), which exercises
+    the pipeline prologue at k > 0."""
+    if nzc:
+        monkeypatch.setenv("TEM_FORCE_NZC", nzc)
     wl = make_workload(name) if name in ("tiny", "block") else WORKLOADS[name]()
     fw, asm, slots, _, sigma, _ = _setup(wl, table=RationalTable([1.0], [[1.0]], [False], [1.0]))
     rng = np.random.default_rng(S)
