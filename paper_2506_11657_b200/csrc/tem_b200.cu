@@ -255,6 +255,7 @@ static void sweep_geometry(const tem_ctx* c, int S, tem::SweepArgs& A, int* grid
   int nzc = 1;
   while (base * nzc < 4 * per_wave && c->g.n[2] / (nzc * 2) >= 16) nzc *= 2;
   if (const char* env = getenv("TEM_FORCE_NZC")) nzc = std::max(1, atoi(env));  // tests
+  nzc = std::max(nzc, (c->g.n[2] + tem::kMaxChunk - 1) / tem::kMaxChunk);
   A.kchunk = (c->g.n[2] + nzc - 1) / nzc;
   A.nzc = (c->g.n[2] + A.kchunk - 1) / A.kchunk;
   *grid = A.ntx * A.nty * A.nzc * S;
@@ -263,9 +264,9 @@ static void sweep_geometry(const tem_ctx* c, int S, tem::SweepArgs& A, int* grid
 static int sweep_attrs() {
   static bool done = false;
   if (done) return TEM_OK;
-  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep_direct<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmem2));
-  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep_direct<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmem2));
-  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep_dirap, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmem1));
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmemDirect));
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmemDirect));
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmemDirap));
   done = true;
   return TEM_OK;
 }
@@ -401,7 +402,7 @@ int tem_apply_shifted(tem_ctx* c, const double* mass, int S, const double* shift
   CUtensorMap tm;
   if (int rc = make_tmap(c, S, x, &tm)) return rc;
   TEM_CUDA(cudaMemsetAsync(y, 0, (size_t)3 * c->g.Nn * S * sizeof(double2), (cudaStream_t)stream));
-  tem::k_sweep_direct<0><<<grid, tem::NT, tem::kSmem2, (cudaStream_t)stream>>>(A, tm);
+  tem::k_sweep<0><<<grid, tem::NT, tem::kSmemDirect, (cudaStream_t)stream>>>(A, tm, tm);
   TEM_CUDA(cudaGetLastError());
   return TEM_OK;
 }
@@ -502,8 +503,8 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
     TEM_CUDA(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
     for (int it = 0; it < kChunk; ++it) {
       const int q = it & 1;
-      tem::k_sweep_dirap<<<grid, tem::NT, tem::kSmem1, c->cap_stream>>>(a1[q], tmZ, tmP[q]);
-      tem::k_sweep_direct<2><<<grid, tem::NT, tem::kSmem2, c->cap_stream>>>(a2[q], tmP[1 - q]);
+      tem::k_sweep<1><<<grid, tem::NT, tem::kSmemDirap, c->cap_stream>>>(a1[q], tmP[q], tmZ);
+      tem::k_sweep<2><<<grid, tem::NT, tem::kSmemDirect, c->cap_stream>>>(a2[q], tmP[1 - q], tmP[1 - q]);
     }
     TEM_CUDA(cudaStreamEndCapture(c->cap_stream, &gr));
     cudaError_t e = cudaGraphInstantiate(&c->graph, gr, 0);
@@ -521,8 +522,8 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
     } else {
       for (int it = 0; it < chunk; ++it) {
         const int q = (done + it) & 1;
-        tem::k_sweep_dirap<<<grid, tem::NT, tem::kSmem1, stream>>>(a1[q], tmZ, tmP[q]);
-        tem::k_sweep_direct<2><<<grid, tem::NT, tem::kSmem2, stream>>>(a2[q], tmP[1 - q]);
+        tem::k_sweep<1><<<grid, tem::NT, tem::kSmemDirap, stream>>>(a1[q], tmP[q], tmZ);
+        tem::k_sweep<2><<<grid, tem::NT, tem::kSmemDirect, stream>>>(a2[q], tmP[1 - q], tmP[1 - q]);
       }
       TEM_CUDA(cudaGetLastError());
     }

@@ -36,12 +36,11 @@ constexpr int TILE_BYTES = HX * HY * 16;  // one plane tile as delivered by TMA 
 constexpr int TILE_STRIDE = (TILE_BYTES + 127) / 128 * 128;   // slot pitch (128 B aligned)
 constexpr int TS2 = TILE_STRIDE / 16;     // slot pitch in double2
 
-// MODE 0/2 ring (direct): sets q = {X(q+1), Y(q+1), Z(q)}; X,Y: 5 slots, Z: 4 slots
-constexpr int R2_XY = 5, R2_Z = 4;
-constexpr size_t kSmem2 = 128 + (size_t)(2 * R2_XY + R2_Z) * TILE_STRIDE;
-// MODE 1: p_new ring X,Y: 4 slots, Z: 3 slots; raw staging: 2 slots x 6 tiles (z, p_old)
-constexpr int R1_XY = 4, R1_Z = 3, R1_ST = 2;
-constexpr size_t kSmem1 = 128 + (size_t)(2 * R1_XY + R1_Z + 6 * R1_ST) * TILE_STRIDE;
+// ring: sets q = {X(q+1), Y(q+1), Z(q)}; X,Y: 5 slots, Z: 4 slots (+ MODE 1 z staging 2 x 3)
+constexpr int R_XY = 5, R_Z = 4;
+constexpr size_t kSmemDirect = 128 + (size_t)(2 * R_XY + R_Z) * TILE_STRIDE;        // 77 KB
+constexpr size_t kSmemDirap = kSmemDirect + (size_t)6 * TILE_STRIDE;              // 110 KB
+constexpr int kMaxChunk = 128;            // max planes per z-chunk (z tables in smem)
 
 struct ShiftState {
   double2 s;        // shift
@@ -202,13 +201,11 @@ struct Edge3 {
   bool f[3];
 };
 
-__device__ __forceinline__ void stencil3(const Grid& g, const Column& C, int k, const double2* Xm,
-                                         const double2* X0, const double2* Xp, const double2* Ym,
-                                         const double2* Y0, const double2* Yp, const double2* Zm,
-                                         const double2* Z0, Edge3& E) {
-  const double ihz = __ldg(g.ih[2] + k);
-  const double ihzm = k >= 1 ? __ldg(g.ih[2] + k - 1) : 0.0;
-  const double hdz = __ldg(g.hdm[2] + k);
+__device__ __forceinline__ void stencil3(const Grid& g, const Column& C, int k, double ihz, double ihzm,
+                                         double hdz, const double2* Xm, const double2* X0,
+                                         const double2* Xp, const double2* Ym, const double2* Y0,
+                                         const double2* Yp, const double2* Zm, const double2* Z0,
+                                         Edge3& E) {
   const int c0 = C.c0;
   E.f[0] = C.in_ij && free_x(g, C.i, C.j, k);
   E.f[1] = C.in_ij && free_y(g, C.i, C.j, k);
@@ -331,33 +328,46 @@ __device__ __forceinline__ void block_coords(const SweepArgs& A, int& s, int& tx
   ke = min(kb + A.kchunk, A.g.n[2]);
 }
 
-// ---------------------------------------------------------------- MODE 0, 2
+// ---------------------------------------------------------------- sweeps
+// One kernel for the three modes.  Plane sets q = {X(q+1), Y(q+1), Z(q)} of
+// the swept vector v live in a ring: X,Y slots q mod 5, Z slots q mod 4,
+// mbarrier q mod 5.  MODE 0/2: v is read as is, three sets run ahead of the
+// arithmetic.  MODE 1: v = p_old is loaded into the ring and z into a 2-slot
+// staging area; when set q has landed it is combined IN PLACE into
+// p_new = z + beta p_old (at the end of step q-1, two sets ahead), so MODE 1
+// needs 20 tiles (110 KB) and also runs 2 CTAs per SM.
 template <int MODE>
-__global__ void __launch_bounds__(NT, 2) k_sweep_direct(const __grid_constant__ SweepArgs A,
-                                                        const __grid_constant__ CUtensorMap tmv) {
+__global__ void __launch_bounds__(NT, 2) k_sweep(const __grid_constant__ SweepArgs A,
+                                                 const __grid_constant__ CUtensorMap tmv,
+                                                 const __grid_constant__ CUtensorMap tmz) {
+  constexpr bool kZ = (MODE == 1);
   extern __shared__ unsigned char smem_raw[];
   double2* ring = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-  double2* rX = ring;                        // [R2_XY] slots
-  double2* rY = ring + R2_XY * TS2;          // [R2_XY]
-  double2* rZ = ring + 2 * R2_XY * TS2;      // [R2_Z]
-  __shared__ __align__(8) uint64_t bar[R2_XY];
+  double2* rX = ring;                        // [R_XY] slots
+  double2* rY = ring + R_XY * TS2;           // [R_XY]
+  double2* rZ = ring + 2 * R_XY * TS2;       // [R_Z]
+  double2* zs = ring + (2 * R_XY + R_Z) * TS2;   // MODE 1 z staging [2][3 tiles]
+  __shared__ __align__(8) uint64_t bar[R_XY];
   __shared__ double red[3 * NT / 32];
+  __shared__ double zih[kMaxChunk + 1];     // ih_z[k] for k = kb-1 .. ke-1
+  __shared__ double zhd[kMaxChunk];         // hdual_z[k]/mu0 for k = kb .. ke-1
 
   const Grid& g = A.g;
   int s, tx0, ty0, kb, ke;
   block_coords(A, s, tx0, ty0, kb, ke);
   const int tid = threadIdx.x;
 
-  double2 sh, alpha;
+  double2 sh, alpha, beta;
   bool live;
   if (MODE == 0) {
     sh = A.shifts[s];
-    alpha = czero();
+    alpha = beta = czero();
     live = true;
   } else {
     const ShiftState& st = A.st[s];
     sh = st.s;
     alpha = st.alpha;
+    beta = st.beta;
     live = st.active != 0;
   }
   double2 acc_c = czero();
@@ -367,32 +377,74 @@ __global__ void __launch_bounds__(NT, 2) k_sweep_direct(const __grid_constant__ 
     const Column C = make_column(g, tx0, ty0);
     const long long vs = (long long)s * 3 * g.Nn;
     const int nx1 = g.n[0] + 1, ny1 = g.n[1] + 1;
-    // set q = {X(q+1), Y(q+1), Z(q)} -> slots q mod 5 (X,Y), q mod 4 (Z); barrier q mod 5.
-    // Set kb-2 carries no Z tile: Z(kb-2) is never read, and with 5 sets in
+    for (int q = tid; q <= ke - kb; q += NT) {
+      const int k = kb - 1 + q;
+      zih[q] = k >= 0 ? __ldg(g.ih[2] + k) : 0.0;
+      if (q < ke - kb) zhd[q] = __ldg(g.hdm[2] + kb + q);
+    }
+    // Set kb-2 carries no Z tile: Z(kb-2) is never read, and with five sets in
     // flight its Z slot is the one set kb+2 fills (two TMAs into one slot race).
     auto issue = [&](int q) {
-      const int sx = pmod(q, R2_XY), sz = pmod(q, R2_Z);
+      const int sx = pmod(q, R_XY), sz = pmod(q, R_Z);
       const bool with_z = q > kb - 2;
-      mbar_expect_tx(&bar[sx], (with_z ? 3 : 2) * TILE_BYTES);
-      tma_tile(rX + sx * TS2, &tmv, 2 * (tx0 - 1), ty0 - 1, q + 1, 0, s, &bar[sx]);
-      tma_tile(rY + sx * TS2, &tmv, 2 * (tx0 - 1), ty0 - 1, q + 1, 1, s, &bar[sx]);
-      if (with_z) tma_tile(rZ + sz * TS2, &tmv, 2 * (tx0 - 1), ty0 - 1, q, 2, s, &bar[sx]);
+      const int ntile = (with_z ? 3 : 2) * (kZ ? 2 : 1);
+      mbar_expect_tx(&bar[sx], ntile * TILE_BYTES);
+      const int cx = 2 * (tx0 - 1), cy = ty0 - 1;
+      tma_tile(rX + sx * TS2, &tmv, cx, cy, q + 1, 0, s, &bar[sx]);
+      tma_tile(rY + sx * TS2, &tmv, cx, cy, q + 1, 1, s, &bar[sx]);
+      if (with_z) tma_tile(rZ + sz * TS2, &tmv, cx, cy, q, 2, s, &bar[sx]);
+      if (kZ) {
+        double2* d = zs + pmod(q, 2) * 3 * TS2;
+        tma_tile(d, &tmz, cx, cy, q + 1, 0, s, &bar[sx]);
+        tma_tile(d + TS2, &tmz, cx, cy, q + 1, 1, s, &bar[sx]);
+        if (with_z) tma_tile(d + 2 * TS2, &tmz, cx, cy, q, 2, s, &bar[sx]);
+      }
     };
-    if (tid == 0) {
-      for (int q = 0; q < R2_XY; ++q) mbar_init(&bar[q], 1);
-      fence_barrier_init();
-    }
-    __syncthreads();
-    if (tid == 0)
-      for (int q = kb - 2; q <= min(kb + 2, ke - 1); ++q) issue(q);
     uint32_t phase = 0;   // bit b = parity of the next wait on bar[b]
     auto wait_set = [&](int q) {
-      const int b = pmod(q, R2_XY);
+      const int b = pmod(q, R_XY);
       mbar_wait(&bar[b], (phase >> b) & 1u);
       phase ^= 1u << b;
     };
-    wait_set(kb - 2);
-    wait_set(kb - 1);
+    // MODE 1: wait for set q and form p_new = z + beta p_old in its ring slots
+    auto combine = [&](int q) {
+      wait_set(q);
+      const double2* d = zs + pmod(q, 2) * 3 * TS2;
+      double2* dX = rX + pmod(q, R_XY) * TS2;
+      double2* dY = rY + pmod(q, R_XY) * TS2;
+      double2* dZ = rZ + pmod(q, R_Z) * TS2;
+      const bool with_z = q > kb - 2;
+      for (int e = tid; e < HX * HY; e += NT) {
+        dX[e] = cfma(beta, dX[e], d[e]);
+        dY[e] = cfma(beta, dY[e], d[TS2 + e]);
+        if (with_z) dZ[e] = cfma(beta, dZ[e], d[2 * TS2 + e]);
+      }
+    };
+    if (tid == 0) {
+      for (int q = 0; q < R_XY; ++q) mbar_init(&bar[q], 1);
+      fence_barrier_init();
+    }
+    __syncthreads();
+    if (!kZ) {
+      if (tid == 0)
+        for (int q = kb - 2; q <= min(kb + 2, ke - 1); ++q) issue(q);
+      wait_set(kb - 2);
+      wait_set(kb - 1);
+    } else {
+      // z staging has 2 slots: sets enter two at a time
+      if (tid == 0) {
+        issue(kb - 2);
+        issue(kb - 1);
+      }
+      for (int q = kb - 2; q <= kb; ++q) {
+        combine(q);
+        __syncthreads();
+        if (tid == 0 && q + 2 <= ke - 1) {
+          fence_proxy_async();
+          issue(q + 2);
+        }
+      }
+    }
 
     // centre operands of step k, loaded one step ahead
     auto node_of = [&](int k) { return ((long long)k * ny1 + C.j) * nx1 + C.i; };
@@ -425,12 +477,13 @@ __global__ void __launch_bounds__(NT, 2) k_sweep_direct(const __grid_constant__ 
         }
       }
       if (k + 1 < ke) load_centre(k + 1);
-      wait_set(k);
+      if (!kZ) wait_set(k);
       Edge3 E;
-      stencil3(g, C, k, rX + pmod(k - 2, R2_XY) * TS2, rX + pmod(k - 1, R2_XY) * TS2,
-               rX + pmod(k, R2_XY) * TS2, rY + pmod(k - 2, R2_XY) * TS2,
-               rY + pmod(k - 1, R2_XY) * TS2, rY + pmod(k, R2_XY) * TS2,
-               rZ + pmod(k - 1, R2_Z) * TS2, rZ + pmod(k, R2_Z) * TS2, E);
+      stencil3(g, C, k, zih[k - kb + 1], zih[k - kb], zhd[k - kb],
+               rX + pmod(k - 2, R_XY) * TS2, rX + pmod(k - 1, R_XY) * TS2,
+               rX + pmod(k, R_XY) * TS2, rY + pmod(k - 2, R_XY) * TS2,
+               rY + pmod(k - 1, R_XY) * TS2, rY + pmod(k, R_XY) * TS2,
+               rZ + pmod(k - 1, R_Z) * TS2, rZ + pmod(k, R_Z) * TS2, E);
       const long long node = node_of(k);
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -439,6 +492,9 @@ __global__ void __launch_bounds__(NT, 2) k_sweep_direct(const __grid_constant__ 
         const double2 q = cfma(sh, cscale(mC[c], E.p[c]), E.q[c]);   // (K + s M) v
         if (MODE == 0) {
           A.out[e] = q;
+        } else if (MODE == 1) {
+          A.out[e] = E.p[c];                 // p_new
+          acc_c = cfma(E.p[c], q, acc_c);    // p^T A p
         } else {
           const double2 D = make_double2(E.kd[c] + mC[c] * sh.x, mC[c] * sh.y);
           A.x[e] = cfma(alpha, E.p[c], xC[c]);
@@ -449,6 +505,8 @@ __global__ void __launch_bounds__(NT, 2) k_sweep_direct(const __grid_constant__ 
           acc_r += rn.x * rn.x + rn.y * rn.y;
         }
       }
+      // MODE 1: set k+1's ring slots held set k-4/k-3 (no longer read): combine it now
+      if (kZ && k + 1 <= ke - 1) combine(k + 1);
       __syncthreads();   // all reads of set k-2 done -> its slots may be refilled
       if (tid == 0 && k + 3 <= ke - 1) {
         fence_proxy_async();
@@ -464,129 +522,6 @@ __global__ void __launch_bounds__(NT, 2) k_sweep_direct(const __grid_constant__ 
   }
   if (!last_block(&A.ctl->ticket[MODE])) return;
   finalize<MODE>(A);
-}
-
-// ---------------------------------------------------------------- MODE 1
-__global__ void __launch_bounds__(NT, 2) k_sweep_dirap(const __grid_constant__ SweepArgs A,
-                                                       const __grid_constant__ CUtensorMap tmz,
-                                                       const __grid_constant__ CUtensorMap tmp) {
-  extern __shared__ unsigned char smem_raw[];
-  double2* base = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-  double2* rX = base;                              // p_new ring [R1_XY]
-  double2* rY = base + R1_XY * TS2;                // [R1_XY]
-  double2* rZ = base + 2 * R1_XY * TS2;            // [R1_Z]
-  double2* stg = base + (2 * R1_XY + R1_Z) * TS2;  // staging [R1_ST][6 tiles]: zX zY zZ pX pY pZ
-  __shared__ __align__(8) uint64_t bar[R1_ST];
-  __shared__ double red[3 * NT / 32];
-
-  const Grid& g = A.g;
-  int s, tx0, ty0, kb, ke;
-  block_coords(A, s, tx0, ty0, kb, ke);
-  const int tid = threadIdx.x;
-
-  const ShiftState& stt = A.st[s];
-  const double2 sh = stt.s;
-  const double2 beta = stt.beta;
-  const bool live = stt.active != 0;
-  double2 acc_c = czero();
-  double acc_r = 0.0;
-
-  if (live) {
-    const Column C = make_column(g, tx0, ty0);
-    const long long vs = (long long)s * 3 * g.Nn;
-    const int nx1 = g.n[0] + 1, ny1 = g.n[1] + 1;
-    // raw set q = z and p_old tiles {X(q+1), Y(q+1), Z(q)} -> staging slot q mod 2
-    auto issue = [&](int q) {
-      const int b = pmod(q, R1_ST);
-      double2* d = stg + b * 6 * TS2;
-      mbar_expect_tx(&bar[b], 6 * TILE_BYTES);
-      tma_tile(d + 0 * TS2, &tmz, 2 * (tx0 - 1), ty0 - 1, q + 1, 0, s, &bar[b]);
-      tma_tile(d + 1 * TS2, &tmz, 2 * (tx0 - 1), ty0 - 1, q + 1, 1, s, &bar[b]);
-      tma_tile(d + 2 * TS2, &tmz, 2 * (tx0 - 1), ty0 - 1, q, 2, s, &bar[b]);
-      tma_tile(d + 3 * TS2, &tmp, 2 * (tx0 - 1), ty0 - 1, q + 1, 0, s, &bar[b]);
-      tma_tile(d + 4 * TS2, &tmp, 2 * (tx0 - 1), ty0 - 1, q + 1, 1, s, &bar[b]);
-      tma_tile(d + 5 * TS2, &tmp, 2 * (tx0 - 1), ty0 - 1, q, 2, s, &bar[b]);
-    };
-    uint32_t phase = 0;
-    // wait raw set q, combine p_new = z + beta p_old into ring slots q mod 4 / q mod 3
-    auto combine = [&](int q) {
-      const int b = pmod(q, R1_ST);
-      mbar_wait(&bar[b], (phase >> b) & 1u);
-      phase ^= 1u << b;
-      const double2* d = stg + b * 6 * TS2;
-      double2* dX = rX + pmod(q, R1_XY) * TS2;
-      double2* dY = rY + pmod(q, R1_XY) * TS2;
-      double2* dZ = rZ + pmod(q, R1_Z) * TS2;
-      for (int e = tid; e < HX * HY; e += NT) {
-        dX[e] = cfma(beta, d[3 * TS2 + e], d[0 * TS2 + e]);
-        dY[e] = cfma(beta, d[4 * TS2 + e], d[1 * TS2 + e]);
-        dZ[e] = cfma(beta, d[5 * TS2 + e], d[2 * TS2 + e]);
-      }
-    };
-    if (tid == 0) {
-      for (int q = 0; q < R1_ST; ++q) mbar_init(&bar[q], 1);
-      fence_barrier_init();
-    }
-    __syncthreads();
-    if (tid == 0) {
-      issue(kb - 2);
-      issue(kb - 1);
-    }
-    // prologue: sets kb-2, kb-1, kb into the ring; raw kb+1, kb+2 left in flight
-    for (int q = kb - 2; q <= kb; ++q) {
-      combine(q);
-      __syncthreads();
-      if (tid == 0 && q + 2 <= ke - 1) {
-        fence_proxy_async();
-        issue(q + 2);
-      }
-    }
-    auto node_of = [&](int k) { return ((long long)k * ny1 + C.j) * nx1 + C.i; };
-    double mN[3];
-    auto load_mass = [&](int k) {
-      const long long node = node_of(k);
-      const bool ok = C.in_ij && k < g.n[2];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) mN[c] = ok ? __ldg(A.mass + (long long)c * g.Nn + node) : 0.0;
-    };
-    load_mass(kb);
-
-    for (int k = kb; k < ke; ++k) {
-      double mC[3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) mC[c] = mN[c];
-      if (k + 1 < ke) load_mass(k + 1);
-      Edge3 E;
-      stencil3(g, C, k, rX + pmod(k - 2, R1_XY) * TS2, rX + pmod(k - 1, R1_XY) * TS2,
-               rX + pmod(k, R1_XY) * TS2, rY + pmod(k - 2, R1_XY) * TS2,
-               rY + pmod(k - 1, R1_XY) * TS2, rY + pmod(k, R1_XY) * TS2,
-               rZ + pmod(k - 1, R1_Z) * TS2, rZ + pmod(k, R1_Z) * TS2, E);
-      const long long node = node_of(k);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        if (!E.f[c]) continue;
-        const long long e = vs + (long long)c * g.Nn + node;
-        const double2 q = cfma(sh, cscale(mC[c], E.p[c]), E.q[c]);
-        A.out[e] = E.p[c];                 // p_new
-        acc_c = cfma(E.p[c], q, acc_c);    // p^T A p
-      }
-      // the ring slots of set k+1 held set k-3 (no longer read): combine the
-      // raw set k+1 there, then refill its staging slot with raw set k+3
-      if (k + 1 <= ke - 1) combine(k + 1);
-      __syncthreads();
-      if (tid == 0 && k + 3 <= ke - 1) {
-        fence_proxy_async();
-        issue(k + 3);
-      }
-    }
-  }
-  block_sum_n<NT>(acc_c, acc_r, red);
-  if (tid == 0) {
-    A.part_c[blockIdx.x] = acc_c;
-    A.part_r[blockIdx.x] = acc_r;
-  }
-  if (!last_block(&A.ctl->ticket[1])) return;
-  finalize<1>(A);
 }
 
 }  // namespace tem
