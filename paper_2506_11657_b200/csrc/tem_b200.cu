@@ -31,6 +31,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -161,7 +162,8 @@ __global__ void __launch_bounds__(256) k_init(tem::SweepArgs A, double2* p0, dou
   __syncthreads();
   if (threadIdx.x == 0) {
     int na = 0;
-    for (int q = 0; q < S; ++q) na += A.st[q].active;
+    for (int q = 0; q < S; ++q)
+      if (A.st[q].active) A.ctl->list[na++] = q;
     A.ctl->n_active = na;
     A.ctl->ticket[0] = 0;
   }
@@ -222,9 +224,10 @@ struct tem_ctx {
   double* dev_h = nullptr;          // ih[3] and hdm[3] packed
   cudaStream_t cap_stream = nullptr;
   int* pinned_active = nullptr;
-  // cached graph of kChunk COCG iterations
-  cudaGraphExec_t graph = nullptr;
-  tem::SweepArgs graph_a1{}, graph_a2{};
+  // cached graphs of kChunk COCG iterations, per (slots, z-chunks), for one set of buffers
+  std::map<long long, cudaGraphExec_t> graphs;
+  std::vector<const void*> graph_key;
+  int graph_S = 0;
   // scratch
   void* scratch = nullptr;          // residues etc.
   size_t scratch_bytes = 0;
@@ -243,22 +246,35 @@ static int check_S(int S) {
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-// sweep geometry: xy tiles x z-chunks x shifts
-static void sweep_geometry(const tem_ctx* c, int S, tem::SweepArgs& A, int* grid) {
+// sweep geometry: xy tiles x z-chunks x shift slots.  The z-range is split
+// until the grid covers ~4 waves of 2 CTAs/SM, so that a few remaining
+// (slow-converging) shifts still fill the machine.
+static void sweep_geometry(const tem_ctx* c, int S, int nslot, tem::SweepArgs& A, int* grid) {
   A.g = c->g;
   A.S = S;
+  A.nslot = nslot;
   A.ntx = (c->g.n[0] + tem::TX - 1) / tem::TX;
   A.nty = (c->g.n[1] + tem::TY - 1) / tem::TY;
-  // split z so that the grid covers the machine several times over
-  const int per_wave = c->num_sms * 2;
-  const int base = A.ntx * A.nty * S;
+  const int target = 4 * c->num_sms * 2;
+  const int base = A.ntx * A.nty * nslot;
   int nzc = 1;
-  while (base * nzc < 4 * per_wave && c->g.n[2] / (nzc * 2) >= 16) nzc *= 2;
+  while (base * nzc < target && c->g.n[2] / (nzc * 2) >= 16) nzc *= 2;
   if (const char* env = getenv("TEM_FORCE_NZC")) nzc = std::max(1, atoi(env));  // tests
   nzc = std::max(nzc, (c->g.n[2] + tem::kMaxChunk - 1) / tem::kMaxChunk);
   A.kchunk = (c->g.n[2] + nzc - 1) / nzc;
   A.nzc = (c->g.n[2] + A.kchunk - 1) / A.kchunk;
-  *grid = A.ntx * A.nty * A.nzc * S;
+  *grid = A.ntx * A.nty * A.nzc * nslot;
+}
+
+static int max_sweep_grid(const tem_ctx* c, int S) {
+  int gmax = 0;
+  for (int ns = 1; ns <= S; ++ns) {
+    tem::SweepArgs A{};
+    int gr = 0;
+    sweep_geometry(c, S, ns, A, &gr);
+    gmax = std::max(gmax, gr);
+  }
+  return gmax;
 }
 
 static int sweep_attrs() {
@@ -362,7 +378,7 @@ int tem_create(int nx, int ny, int nz, const double* hx, const double* hy, const
 
 void tem_destroy(tem_ctx* c) {
   if (!c) return;
-  if (c->graph) cudaGraphExecDestroy(c->graph);
+  for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
   if (c->dev_h) cudaFree(c->dev_h);
   if (c->scratch) cudaFree(c->scratch);
   if (c->e2e) cudaFree(c->e2e);
@@ -395,7 +411,7 @@ int tem_apply_shifted(tem_ctx* c, const double* mass, int S, const double* shift
   if (int rc = check_S(S)) return rc;
   tem::SweepArgs A{};
   int grid = 0;
-  sweep_geometry(c, S, A, &grid);
+  sweep_geometry(c, S, S, A, &grid);
   for (int s = 0; s < S; ++s) A.shifts[s] = make_double2(shifts[2 * s], shifts[2 * s + 1]);
   A.mass = mass;
   A.out = reinterpret_cast<double2*>(y);
@@ -414,10 +430,7 @@ struct WorkLayout {
 static WorkLayout work_layout(const tem_ctx* c, int S) {
   WorkLayout L{};
   const size_t vec = (size_t)3 * c->g.Nn * S * sizeof(double2);
-  tem::SweepArgs A{};
-  int grid = 0;
-  sweep_geometry(c, S, A, &grid);
-  const size_t nparts = (size_t)std::max(grid, 1024 * S);
+  const size_t nparts = (size_t)std::max(max_sweep_grid(c, S), 1024 * S);
   size_t o = 0;
   L.z = o;      o = align_up(o + vec, 256);
   L.p0 = o;     o = align_up(o + vec, 256);
@@ -435,11 +448,6 @@ size_t tem_cocg_workspace_bytes(const tem_ctx* c, int S) {
   return work_layout(c, S).total;
 }
 
-static bool same_args(const tem::SweepArgs& a, const tem::SweepArgs& b) {
-  return a.S == b.S && a.mass == b.mass && a.out == b.out && a.x == b.x && a.z == b.z && a.st == b.st && a.ctl == b.ctl && a.part_c == b.part_c &&
-         a.part_r == b.part_r && a.g.Nn == b.g.Nn && a.g.ih[0] == b.g.ih[0] && a.nzc == b.nzc;
-}
-
 int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const double* shifts,
                    double tol, int maxit, double* x, void* work, size_t work_bytes, int* iters,
                    double* relres, void* stream_) {
@@ -453,7 +461,7 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
 
   tem::SweepArgs base{};
   int grid = 0;
-  sweep_geometry(c, S, base, &grid);
+  sweep_geometry(c, S, S, base, &grid);
   base.mass = mass;
   base.x = reinterpret_cast<double2*>(x);
   base.z = reinterpret_cast<double2*>(w + L.z);
@@ -462,16 +470,59 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
   base.part_c = reinterpret_cast<double2*>(w + L.part_c);
   base.part_r = reinterpret_cast<double*>(w + L.part_r);
   double2* P[2] = {reinterpret_cast<double2*>(w + L.p0), reinterpret_cast<double2*>(w + L.p1)};
-  // iteration parity q: sweep 1 reads p_old = P[q], writes p_new = P[1-q]; sweep 2 reads P[1-q]
-  tem::SweepArgs a1[2], a2[2];
   CUtensorMap tmP[2], tmZ;
-  for (int q = 0; q < 2; ++q) {
-    a1[q] = base;
-    a1[q].out = P[1 - q];
-    a2[q] = base;
+  for (int q = 0; q < 2; ++q)
     if (int rc = make_tmap(c, S, P[q], &tmP[q])) return rc;
-  }
   if (int rc = make_tmap(c, S, base.z, &tmZ)) return rc;
+
+  // iteration parity q: sweep 1 reads p_old = P[q], writes p_new = P[1-q];
+  // sweep 2 reads P[1-q].  Launch configuration for `nslot` active shifts.
+  struct Cfg {
+    tem::SweepArgs a1[2], a2[2];
+    int grid;
+  };
+  auto make_cfg = [&](int nslot) {
+    Cfg k{};
+    tem::SweepArgs g0 = base;
+    sweep_geometry(c, S, nslot, g0, &k.grid);
+    for (int q = 0; q < 2; ++q) {
+      k.a1[q] = g0;
+      k.a1[q].out = P[1 - q];
+      k.a2[q] = g0;
+    }
+    return k;
+  };
+  auto launch_iter = [&](const Cfg& k, int q, cudaStream_t st_) {
+    tem::k_sweep<1><<<k.grid, tem::NT, tem::kSmemDirap, st_>>>(k.a1[q], tmP[q], tmZ);
+    tem::k_sweep<2><<<k.grid, tem::NT, tem::kSmemDirect, st_>>>(k.a2[q], tmP[1 - q], tmP[1 - q]);
+  };
+  // graphs of kChunk iterations, cached per (slots, z-chunks) for these buffers
+  const std::vector<const void*> key = {mass, x, work, f};
+  if (c->graph_key != key || c->graph_S != S) {
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    c->graphs.clear();
+    c->graph_key = key;
+    c->graph_S = S;
+  }
+  auto get_graph = [&](const Cfg& k, int nslot, cudaGraphExec_t* out) -> int {
+    const long long id = (long long)nslot * 4096 + k.a1[0].nzc;
+    auto it = c->graphs.find(id);
+    if (it != c->graphs.end()) {
+      *out = it->second;
+      return TEM_OK;
+    }
+    cudaGraph_t gr;
+    TEM_CUDA(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < kChunk; ++i) launch_iter(k, i & 1, c->cap_stream);
+    TEM_CUDA(cudaStreamEndCapture(c->cap_stream, &gr));
+    cudaGraphExec_t ex;
+    cudaError_t e = cudaGraphInstantiate(&ex, gr, 0);
+    cudaGraphDestroy(gr);
+    if (e != cudaSuccess) return fail(TEM_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    c->graphs[id] = ex;
+    *out = ex;
+    return TEM_OK;
+  };
 
   // per-shift state + control (host -> device, small)
   std::vector<tem::ShiftState> st(S);
@@ -493,38 +544,18 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
   TEM_CUDA(cudaGetLastError());
   long long launches = 1;
 
-  const bool same = c->graph && same_args(c->graph_a1, a1[0]) && same_args(c->graph_a2, a2[0]);
-  if (!same) {
-    if (c->graph) {
-      cudaGraphExecDestroy(c->graph);
-      c->graph = nullptr;
-    }
-    cudaGraph_t gr;
-    TEM_CUDA(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
-    for (int it = 0; it < kChunk; ++it) {
-      const int q = it & 1;
-      tem::k_sweep<1><<<grid, tem::NT, tem::kSmemDirap, c->cap_stream>>>(a1[q], tmP[q], tmZ);
-      tem::k_sweep<2><<<grid, tem::NT, tem::kSmemDirect, c->cap_stream>>>(a2[q], tmP[1 - q], tmP[1 - q]);
-    }
-    TEM_CUDA(cudaStreamEndCapture(c->cap_stream, &gr));
-    cudaError_t e = cudaGraphInstantiate(&c->graph, gr, 0);
-    cudaGraphDestroy(gr);
-    if (e != cudaSuccess) return fail(TEM_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
-    c->graph_a1 = a1[0];
-    c->graph_a2 = a2[0];
-  }
   int done = 0;
   int n_active = S;
+  int nslot = S;
+  Cfg cfg = make_cfg(nslot);
+  cudaGraphExec_t graph = nullptr;
+  if (int rc = get_graph(cfg, nslot, &graph)) return rc;
   while (done < maxit) {
     const int chunk = std::min(kChunk, maxit - done);
     if (chunk == kChunk) {  // kChunk is even: parity returns to 0
-      TEM_CUDA(cudaGraphLaunch(c->graph, stream));
+      TEM_CUDA(cudaGraphLaunch(graph, stream));
     } else {
-      for (int it = 0; it < chunk; ++it) {
-        const int q = (done + it) & 1;
-        tem::k_sweep<1><<<grid, tem::NT, tem::kSmemDirap, stream>>>(a1[q], tmP[q], tmZ);
-        tem::k_sweep<2><<<grid, tem::NT, tem::kSmemDirect, stream>>>(a2[q], tmP[1 - q], tmP[1 - q]);
-      }
+      for (int i = 0; i < chunk; ++i) launch_iter(cfg, (done + i) & 1, stream);
       TEM_CUDA(cudaGetLastError());
     }
     launches += 2LL * chunk;
@@ -533,6 +564,11 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
     TEM_CUDA(cudaStreamSynchronize(stream));
     n_active = *c->pinned_active;
     if (n_active == 0) break;
+    if (n_active < nslot) {  // shifts converged: fewer slots, possibly more z-chunks
+      nslot = n_active;
+      cfg = make_cfg(nslot);
+      if (int rc = get_graph(cfg, nslot, &graph)) return rc;
+    }
   }
   TEM_CUDA(cudaEventRecord(ev1, stream));
   TEM_CUDA(cudaMemcpyAsync(st.data(), base.st, sizeof(tem::ShiftState) * S, cudaMemcpyDeviceToHost, stream));
@@ -557,7 +593,7 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
   c->stats.kernel_launches = launches;
   c->stats.shift_iterations = shift_iters;
   c->stats.iterations = max_it;
-  c->stats.grid = grid;
+  c->stats.grid = grid;   // with all shifts active
   c->stats.block = tem::NT;
   if (status == TEM_EBREAKDOWN) return fail(status, "tem_cocg_solve: COCG breakdown");
   if (status == TEM_ENOCONV) return fail(status, "tem_cocg_solve: not converged within maxit");

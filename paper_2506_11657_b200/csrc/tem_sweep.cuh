@@ -57,13 +57,15 @@ struct ShiftState {
 
 struct Control {
   double tol;
-  int n_active;
+  int n_active;           // number of active shifts
   unsigned int ticket[4];
+  int list[32];           // the active shifts, compacted (first n_active entries)
 };
 
 struct SweepArgs {
   Grid g;
   int S;
+  int nslot;                   // shift slots of the grid (CTA slot a serves shift list[a])
   int ntx, nty, nzc, kchunk;   // tiles along x, y; z-chunks and their length
   const double* mass;          // [3][Nn]
   double2* out;                // MODE 0: y; MODE 1: p_new
@@ -259,18 +261,20 @@ __device__ __forceinline__ void stencil3(const Grid& g, const Column& C, int k, 
 #undef T_
 }
 
-// Finalisation by the last CTA: per-shift sums of the per-CTA partials
-// (CTAs of shift q are blockIdx = q mod S), scalar updates of COCG.
+// Finalisation by the last CTA: per-shift sums of the per-CTA partials (the
+// CTAs of slot a are blockIdx = a mod nslot and served shift list[a]), COCG
+// scalar updates, then the compacted active list for the next launch.
 template <int MODE>
 __device__ void finalize(const SweepArgs& A) {
-  const int S = A.S;
+  const int S = A.S, ns = A.nslot;
+  const int n_list = A.ctl->n_active;   // as read by every CTA of this launch
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nblk = gridDim.x;
-  for (int q = warp; q < S; q += NT / 32) {
-    ShiftState& sq = A.st[q];
+  for (int a = warp; a < ns && a < n_list; a += NT / 32) {
+    ShiftState& sq = A.st[A.ctl->list[a]];
     if (!sq.active) continue;
     double cx = 0, cy = 0, cr = 0;
-    for (int b = q + lane * S; b < nblk; b += 32 * S) {
+    for (int b = a + lane * ns; b < nblk; b += 32 * ns) {
       const double2 v = __ldcg(A.part_c + b);
       cx += v.x;
       cy += v.y;
@@ -308,20 +312,21 @@ __device__ void finalize(const SweepArgs& A) {
   __syncthreads();
   if (threadIdx.x == 0) {
     int na = 0;
-    for (int q = 0; q < S; ++q) na += A.st[q].active;
+    for (int q = 0; q < S; ++q)
+      if (A.st[q].active) A.ctl->list[na++] = q;
     A.ctl->n_active = na;
     A.ctl->ticket[MODE] = 0;
   }
 }
 
-__device__ __forceinline__ void block_coords(const SweepArgs& A, int& s, int& tx0, int& ty0, int& kb,
+__device__ __forceinline__ void block_coords(const SweepArgs& A, int& a, int& tx0, int& ty0, int& kb,
                                              int& ke) {
-  // block -> (z-chunk, xy tile, shift), shift fastest so that the S CTAs of a
-  // tile run together and share its coefficients through L2
-  const int S = A.S;
-  s = blockIdx.x % S;
-  const int xy = (blockIdx.x / S) % (A.ntx * A.nty);
-  const int zc = blockIdx.x / (S * A.ntx * A.nty);
+  // block -> (z-chunk, xy tile, shift slot), slot fastest so that the CTAs of
+  // one tile for all shifts run together and share its coefficients via L2
+  const int ns = A.nslot;
+  a = blockIdx.x % ns;
+  const int xy = (blockIdx.x / ns) % (A.ntx * A.nty);
+  const int zc = blockIdx.x / (ns * A.ntx * A.nty);
   tx0 = (xy % A.ntx) * TX;
   ty0 = (xy / A.ntx) * TY;
   kb = zc * A.kchunk;
@@ -353,22 +358,26 @@ __global__ void __launch_bounds__(NT, 2) k_sweep(const __grid_constant__ SweepAr
   __shared__ double zhd[kMaxChunk];         // hdual_z[k]/mu0 for k = kb .. ke-1
 
   const Grid& g = A.g;
-  int s, tx0, ty0, kb, ke;
-  block_coords(A, s, tx0, ty0, kb, ke);
+  int a, tx0, ty0, kb, ke;
+  block_coords(A, a, tx0, ty0, kb, ke);
   const int tid = threadIdx.x;
 
-  double2 sh, alpha, beta;
+  double2 sh = czero(), alpha = czero(), beta = czero();
   bool live;
+  int s = a;
   if (MODE == 0) {
     sh = A.shifts[s];
-    alpha = beta = czero();
     live = true;
   } else {
-    const ShiftState& st = A.st[s];
-    sh = st.s;
-    alpha = st.alpha;
-    beta = st.beta;
-    live = st.active != 0;
+    live = a < A.ctl->n_active;
+    if (live) {
+      s = A.ctl->list[a];
+      const ShiftState& st = A.st[s];
+      sh = st.s;
+      alpha = st.alpha;
+      beta = st.beta;
+      live = st.active != 0;
+    }
   }
   double2 acc_c = czero();
   double acc_r = 0.0;
