@@ -101,6 +101,22 @@ def _dist_env():
     return ws, rank, local
 
 
+def reduce_job(times, work, device=None):
+    """Whole-job aggregation across ranks: elapsed times -> MAX over ranks
+    (the job ends when the slowest rank ends), work counts -> SUM.  No-op on a
+    single process.  Tensors live on `device` (cuda for NCCL, cpu for gloo)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return list(times), list(work)
+    dev = device or ("cuda" if dist.get_backend() == "nccl" else "cpu")
+    t = torch.tensor([float(v) for v in times], dtype=torch.float64, device=dev)
+    w = torch.tensor([float(v) for v in work], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(w, op=dist.ReduceOp.SUM)
+    return [float(v) for v in t.tolist()], [int(round(v)) for v in w.tolist()]
+
+
 def _workload_for_rank(name: str, rank: int):
     from workloads import make_workload
     from workloads.configs import loop_source_edges
@@ -175,13 +191,7 @@ def run_ours(args):
     assert np.all(relres <= args.tol), relres
 
     # max over ranks for the time, sums for the work
-    t_max, sui_tot, loop_max = ms, sui, loop_ms
-    if ws > 1:
-        tt = torch.tensor([ms, loop_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        w = torch.tensor([float(sui)], dtype=torch.float64, device=dev)
-        dist.all_reduce(w, op=dist.ReduceOp.SUM)
-        t_max, loop_max, sui_tot = float(tt[0]), float(tt[1]), int(w.item())
+    (t_max, loop_max), (sui_tot,) = reduce_job([ms, loop_ms], [sui], dev)
 
     # ---- e2e through the C ABI with pinned host buffers (rank-local, then max)
     e2e = None
@@ -200,13 +210,7 @@ def run_ours(args):
             e2e_sui += int(np.sum(it_h)) * N
         barrier()
         e2e_s = time.perf_counter() - t0
-        if ws > 1:
-            tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_s = float(tt.item())
-            w = torch.tensor([float(e2e_sui)], dtype=torch.float64, device=dev)
-            dist.all_reduce(w, op=dist.ReduceOp.SUM)
-            e2e_sui = int(w.item())
+        (e2e_s,), (e2e_sui,) = reduce_job([e2e_s], [e2e_sui], dev)
         e2e = {"value": e2e_sui / e2e_s, "unit": "shift-unknown-iterations/s",
                "h2d_bytes_per_step": int(sig_h.numel() * 8 + f_h.numel() * 8),
                "d2h_bytes_per_step": int(u_h.numel() * 8),
@@ -249,7 +253,7 @@ def run_ours(args):
                    "parallelism": f"{ws} independent soundings" if ws > 1 else "1 GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "COCG sweeps (k_dir + k_ap + k_upd), algorithmic 128 B/SUI",
+                     "kernel": "COCG sweeps k_sweep<1> + k_sweep<2>, algorithmic 128 B/SUI",
                      "peak_kind": peak_kind},
         "clocks": clk.summary(),
         "e2e": e2e,
