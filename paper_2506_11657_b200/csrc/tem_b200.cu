@@ -31,6 +31,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <map>
 #include <string>
 #include <vector>
@@ -304,9 +305,16 @@ static int make_tmap(const tem_ctx* c, int S, const void* base, CUtensorMap* tm)
   const cuuint64_t strides[4] = {16 * nx1, 16 * nx1 * ny1, 16 * nx1 * ny1 * nz1, 48 * nx1 * ny1 * nz1};
   const cuuint32_t box[5] = {2 * tem::HX, tem::HY, 1, 1, 1};
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  if (const char* env = getenv("TEM_L2PROMO")) {  // experiments
+    const int v = atoi(env);
+    promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+          : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+          : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
   CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<void*>(base), dims, strides,
                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                      promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(TEM_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return TEM_OK;
 }
@@ -544,6 +552,8 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
   TEM_CUDA(cudaGetLastError());
   long long launches = 1;
 
+  const bool trace = getenv("TEM_TRACE") != nullptr;
+  auto t_prev = std::chrono::steady_clock::now();
   int done = 0;
   int n_active = S;
   int nslot = S;
@@ -563,6 +573,13 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
     TEM_CUDA(cudaMemcpyAsync(c->pinned_active, &base.ctl->n_active, sizeof(int), cudaMemcpyDeviceToHost, stream));
     TEM_CUDA(cudaStreamSynchronize(stream));
     n_active = *c->pinned_active;
+    if (trace) {
+      const auto now = std::chrono::steady_clock::now();
+      fprintf(stderr, "[tem trace] it=%d slots=%d nzc=%d grid=%d active=%d chunk_ms=%.3f\n", done, nslot,
+              cfg.a1[0].nzc, cfg.grid, n_active,
+              std::chrono::duration<double, std::milli>(now - t_prev).count());
+      t_prev = now;
+    }
     if (n_active == 0) break;
     if (n_active < nslot) {  // shifts converged: fewer slots, possibly more z-chunks
       nslot = n_active;

@@ -172,11 +172,14 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Column constants of thread (i, j) of the tile.
+// Column constants of thread (i, j) of the tile: products of inverse cell
+// widths and dual lengths that do not depend on k.
 struct Column {
   int i, j, c0;
   bool in_ij;
-  double ihx, ihxm, ihy, ihym, hdx, hdy;
+  double pxy, pxym, pxmy;   // ih_x ih_y, ih_x ih_y(j-1), ih_x(i-1) ih_y
+  double cyx, cyxm;         // hd_y ih_x, hd_y ih_x(i-1)
+  double cxy, cxym;         // hd_x ih_y, hd_x ih_y(j-1)
 };
 
 __device__ __forceinline__ Column make_column(const Grid& g, int tx0, int ty0) {
@@ -186,17 +189,28 @@ __device__ __forceinline__ Column make_column(const Grid& g, int tx0, int ty0) {
   C.j = ty0 + (tid / TX);
   C.c0 = ((tid / TX) + 1) * HX + (tid % TX) + 1;
   C.in_ij = C.i < g.n[0] && C.j < g.n[1];
-  C.ihx = C.in_ij ? __ldg(g.ih[0] + C.i) : 0.0;
-  C.ihxm = (C.in_ij && C.i >= 1) ? __ldg(g.ih[0] + C.i - 1) : 0.0;
-  C.ihy = C.in_ij ? __ldg(g.ih[1] + C.j) : 0.0;
-  C.ihym = (C.in_ij && C.j >= 1) ? __ldg(g.ih[1] + C.j - 1) : 0.0;
-  C.hdx = C.in_ij ? __ldg(g.hdm[0] + C.i) : 0.0;
-  C.hdy = C.in_ij ? __ldg(g.hdm[1] + C.j) : 0.0;
+  const double ihx = C.in_ij ? __ldg(g.ih[0] + C.i) : 0.0;
+  const double ihxm = (C.in_ij && C.i >= 1) ? __ldg(g.ih[0] + C.i - 1) : 0.0;
+  const double ihy = C.in_ij ? __ldg(g.ih[1] + C.j) : 0.0;
+  const double ihym = (C.in_ij && C.j >= 1) ? __ldg(g.ih[1] + C.j - 1) : 0.0;
+  const double hdx = C.in_ij ? __ldg(g.hdm[0] + C.i) : 0.0;
+  const double hdy = C.in_ij ? __ldg(g.hdm[1] + C.j) : 0.0;
+  C.pxy = ihx * ihy;
+  C.pxym = ihx * ihym;
+  C.pxmy = ihxm * ihy;
+  C.cyx = hdy * ihx;
+  C.cyxm = hdy * ihxm;
+  C.cxy = hdx * ihy;
+  C.cxym = hdx * ihym;
   return C;
 }
 
 // K v for the three edges of node (i, j, k) from ring tiles:
 // Xm/X0/Xp = x-comp planes k-1/k/k+1, same for Y; Zm/Z0 = z-comp layers k-1/k.
+// The 12 (edge, face) pairs touch only 9 distinct faces and 24 distinct tile
+// values: each face circulation F is formed once, scaled by its weight
+// W = hdual/(mu0 A) (G = W F), and the edges combine G's with the incidence
+// signs of K = T^T W T.
 struct Edge3 {
   double2 q[3], p[3];
   double kd[3];
@@ -213,52 +227,42 @@ __device__ __forceinline__ void stencil3(const Grid& g, const Column& C, int k, 
   E.f[1] = C.in_ij && free_y(g, C.i, C.j, k);
   E.f[2] = C.in_ij && free_z(g, C.i, C.j, k);
 #define T_(P, di, dj) P[c0 + (dj) * HX + (di)]
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    E.q[c] = czero();
-    E.p[c] = czero();
-    E.kd[c] = 0.0;
-  }
-  if (E.f[0]) {  // x-edge: A=x, B=y, D=z
-    const double2 a0 = T_(X0, 0, 0);
-    const double2 cD0 = csub(cadd(a0, T_(Y0, 1, 0)), cadd(T_(X0, 0, 1), T_(Y0, 0, 0)));
-    const double2 cD1 = csub(cadd(T_(X0, 0, -1), T_(Y0, 1, -1)), cadd(a0, T_(Y0, 0, -1)));
-    const double2 cB0 = csub(cadd(T_(Z0, 0, 0), T_(Xp, 0, 0)), cadd(T_(Z0, 1, 0), a0));
-    const double2 cB1 = csub(cadd(T_(Zm, 0, 0), a0), cadd(T_(Zm, 1, 0), T_(Xm, 0, 0)));
-    const double wD0 = hdz * C.ihx * C.ihy, wD1 = hdz * C.ihx * C.ihym;
-    const double wB0 = C.hdy * C.ihx * ihz, wB1 = C.hdy * C.ihx * ihzm;
-    E.q[0] = make_double2(wD0 * cD0.x - wD1 * cD1.x - wB0 * cB0.x + wB1 * cB1.x,
-                          wD0 * cD0.y - wD1 * cD1.y - wB0 * cB0.y + wB1 * cB1.y);
-    E.kd[0] = wD0 + wD1 + wB0 + wB1;
-    E.p[0] = a0;
-  }
-  if (E.f[1]) {  // y-edge: A=y, B=z, D=x
-    const double2 a0 = T_(Y0, 0, 0);
-    const double2 cD0 = csub(cadd(a0, T_(Z0, 0, 1)), cadd(T_(Yp, 0, 0), T_(Z0, 0, 0)));
-    const double2 cD1 = csub(cadd(T_(Ym, 0, 0), T_(Zm, 0, 1)), cadd(a0, T_(Zm, 0, 0)));
-    const double2 cB0 = csub(cadd(T_(X0, 0, 0), T_(Y0, 1, 0)), cadd(T_(X0, 0, 1), a0));
-    const double2 cB1 = csub(cadd(T_(X0, -1, 0), a0), cadd(T_(X0, -1, 1), T_(Y0, -1, 0)));
-    const double wD0 = C.hdx * C.ihy * ihz, wD1 = C.hdx * C.ihy * ihzm;
-    const double wB0 = hdz * C.ihy * C.ihx, wB1 = hdz * C.ihy * C.ihxm;
-    E.q[1] = make_double2(wD0 * cD0.x - wD1 * cD1.x - wB0 * cB0.x + wB1 * cB1.x,
-                          wD0 * cD0.y - wD1 * cD1.y - wB0 * cB0.y + wB1 * cB1.y);
-    E.kd[1] = wD0 + wD1 + wB0 + wB1;
-    E.p[1] = a0;
-  }
-  if (E.f[2]) {  // z-edge: A=z, B=x, D=y
-    const double2 a0 = T_(Z0, 0, 0);
-    const double2 cD0 = csub(cadd(a0, T_(Xp, 0, 0)), cadd(T_(Z0, 1, 0), T_(X0, 0, 0)));
-    const double2 cD1 = csub(cadd(T_(Z0, -1, 0), T_(Xp, -1, 0)), cadd(a0, T_(X0, -1, 0)));
-    const double2 cB0 = csub(cadd(T_(Y0, 0, 0), T_(Z0, 0, 1)), cadd(T_(Yp, 0, 0), a0));
-    const double2 cB1 = csub(cadd(T_(Y0, 0, -1), a0), cadd(T_(Yp, 0, -1), T_(Z0, 0, -1)));
-    const double wD0 = C.hdy * ihz * C.ihx, wD1 = C.hdy * ihz * C.ihxm;
-    const double wB0 = C.hdx * ihz * C.ihy, wB1 = C.hdx * ihz * C.ihym;
-    E.q[2] = make_double2(wD0 * cD0.x - wD1 * cD1.x - wB0 * cB0.x + wB1 * cB1.x,
-                          wD0 * cD0.y - wD1 * cD1.y - wB0 * cB0.y + wB1 * cB1.y);
-    E.kd[2] = wD0 + wD1 + wB0 + wB1;
-    E.p[2] = a0;
-  }
+  // 24 tile values
+  const double2 x00 = T_(X0, 0, 0), x01 = T_(X0, 0, 1), x0m = T_(X0, 0, -1);
+  const double2 xm0 = T_(X0, -1, 0), xm1 = T_(X0, -1, 1);
+  const double2 y00 = T_(Y0, 0, 0), y10 = T_(Y0, 1, 0), y1m = T_(Y0, 1, -1);
+  const double2 y0m = T_(Y0, 0, -1), ym0 = T_(Y0, -1, 0);
+  const double2 z00 = T_(Z0, 0, 0), z10 = T_(Z0, 1, 0), z01 = T_(Z0, 0, 1);
+  const double2 zm0 = T_(Z0, -1, 0), z0m = T_(Z0, 0, -1);
+  const double2 xp00 = T_(Xp, 0, 0), xpm0 = T_(Xp, -1, 0), xm00 = T_(Xm, 0, 0);
+  const double2 yp00 = T_(Yp, 0, 0), yp0m = T_(Yp, 0, -1), ym00 = T_(Ym, 0, 0);
+  const double2 zl00 = T_(Zm, 0, 0), zl10 = T_(Zm, 1, 0), zl01 = T_(Zm, 0, 1);
 #undef T_
+  // face weights W = hdual / (mu0 A)
+  const double wz = hdz * C.pxy, wz_y = hdz * C.pxym, wz_x = hdz * C.pxmy;      // Fz(m), Fz(m-ey), Fz(m-ex)
+  const double wy = C.cyx * ihz, wy_z = C.cyx * ihzm, wy_x = C.cyxm * ihz;      // Fy(m), Fy(m-ez), Fy(m-ex)
+  const double wx = C.cxy * ihz, wx_z = C.cxy * ihzm, wx_y = C.cxym * ihz;      // Fx(m), Fx(m-ez), Fx(m-ey)
+  // G = W * circulation (right-hand rule about the face normal)
+  const double2 Gz = cscale(wz, csub(cadd(x00, y10), cadd(x01, y00)));
+  const double2 Gz_y = cscale(wz_y, csub(cadd(x0m, y1m), cadd(x00, y0m)));
+  const double2 Gz_x = cscale(wz_x, csub(cadd(xm0, y00), cadd(xm1, ym0)));
+  const double2 Gy = cscale(wy, csub(cadd(z00, xp00), cadd(z10, x00)));
+  const double2 Gy_z = cscale(wy_z, csub(cadd(zl00, x00), cadd(zl10, xm00)));
+  const double2 Gy_x = cscale(wy_x, csub(cadd(zm0, xpm0), cadd(z00, xm0)));
+  const double2 Gx = cscale(wx, csub(cadd(y00, z01), cadd(yp00, z00)));
+  const double2 Gx_z = cscale(wx_z, csub(cadd(ym00, zl01), cadd(y00, zl00)));
+  const double2 Gx_y = cscale(wx_y, csub(cadd(y0m, z00), cadd(yp0m, z0m)));
+  // (K v)_x = Gz - Gz(m-ey) - Gy + Gy(m-ez); (K v)_y = Gx - Gx(m-ez) - Gz + Gz(m-ex);
+  // (K v)_z = Gy - Gy(m-ex) - Gx + Gx(m-ey)
+  E.q[0] = csub(cadd(Gz, Gy_z), cadd(Gz_y, Gy));
+  E.q[1] = csub(cadd(Gx, Gz_x), cadd(Gx_z, Gz));
+  E.q[2] = csub(cadd(Gy, Gx_y), cadd(Gy_x, Gx));
+  E.kd[0] = wz + wz_y + wy + wy_z;
+  E.kd[1] = wx + wx_z + wz + wz_x;
+  E.kd[2] = wy + wy_x + wx + wx_y;
+  E.p[0] = x00;
+  E.p[1] = y00;
+  E.p[2] = z00;
 }
 
 // Finalisation by the last CTA: per-shift sums of the per-CTA partials (the
