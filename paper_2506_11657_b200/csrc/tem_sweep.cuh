@@ -227,36 +227,40 @@ __device__ __forceinline__ void stencil3(const Grid& g, const Column& C, int k, 
   E.f[1] = C.in_ij && free_y(g, C.i, C.j, k);
   E.f[2] = C.in_ij && free_z(g, C.i, C.j, k);
 #define T_(P, di, dj) P[c0 + (dj) * HX + (di)]
-  // 24 tile values
-  const double2 x00 = T_(X0, 0, 0), x01 = T_(X0, 0, 1), x0m = T_(X0, 0, -1);
-  const double2 xm0 = T_(X0, -1, 0), xm1 = T_(X0, -1, 1);
-  const double2 y00 = T_(Y0, 0, 0), y10 = T_(Y0, 1, 0), y1m = T_(Y0, 1, -1);
-  const double2 y0m = T_(Y0, 0, -1), ym0 = T_(Y0, -1, 0);
-  const double2 z00 = T_(Z0, 0, 0), z10 = T_(Z0, 1, 0), z01 = T_(Z0, 0, 1);
-  const double2 zm0 = T_(Z0, -1, 0), z0m = T_(Z0, 0, -1);
-  const double2 xp00 = T_(Xp, 0, 0), xpm0 = T_(Xp, -1, 0), xm00 = T_(Xm, 0, 0);
-  const double2 yp00 = T_(Yp, 0, 0), yp0m = T_(Yp, 0, -1), ym00 = T_(Ym, 0, 0);
-  const double2 zl00 = T_(Zm, 0, 0), zl10 = T_(Zm, 1, 0), zl01 = T_(Zm, 0, 1);
-#undef T_
+  const double2 x00 = T_(X0, 0, 0), y00 = T_(Y0, 0, 0), z00 = T_(Z0, 0, 0);
   // face weights W = hdual / (mu0 A)
   const double wz = hdz * C.pxy, wz_y = hdz * C.pxym, wz_x = hdz * C.pxmy;      // Fz(m), Fz(m-ey), Fz(m-ex)
   const double wy = C.cyx * ihz, wy_z = C.cyx * ihzm, wy_x = C.cyxm * ihz;      // Fy(m), Fy(m-ez), Fy(m-ex)
   const double wx = C.cxy * ihz, wx_z = C.cxy * ihzm, wx_y = C.cxym * ihz;      // Fx(m), Fx(m-ez), Fx(m-ey)
-  // G = W * circulation (right-hand rule about the face normal)
-  const double2 Gz = cscale(wz, csub(cadd(x00, y10), cadd(x01, y00)));
-  const double2 Gz_y = cscale(wz_y, csub(cadd(x0m, y1m), cadd(x00, y0m)));
-  const double2 Gz_x = cscale(wz_x, csub(cadd(xm0, y00), cadd(xm1, ym0)));
-  const double2 Gy = cscale(wy, csub(cadd(z00, xp00), cadd(z10, x00)));
-  const double2 Gy_z = cscale(wy_z, csub(cadd(zl00, x00), cadd(zl10, xm00)));
-  const double2 Gy_x = cscale(wy_x, csub(cadd(zm0, xpm0), cadd(z00, xm0)));
-  const double2 Gx = cscale(wx, csub(cadd(y00, z01), cadd(yp00, z00)));
-  const double2 Gx_z = cscale(wx_z, csub(cadd(ym00, zl01), cadd(y00, zl00)));
-  const double2 Gx_y = cscale(wx_y, csub(cadd(y0m, z00), cadd(yp0m, z0m)));
-  // (K v)_x = Gz - Gz(m-ey) - Gy + Gy(m-ez); (K v)_y = Gx - Gx(m-ez) - Gz + Gz(m-ex);
-  // (K v)_z = Gy - Gy(m-ex) - Gx + Gx(m-ey)
-  E.q[0] = csub(cadd(Gz, Gy_z), cadd(Gz_y, Gy));
-  E.q[1] = csub(cadd(Gx, Gz_x), cadd(Gx_z, Gz));
-  E.q[2] = csub(cadd(Gy, Gx_y), cadd(Gy_x, Gx));
+  // G = W * circulation (right-hand rule about the face normal), accumulated
+  // into (K v)_x = Gz - Gz(m-ey) - Gy + Gy(m-ez), (K v)_y = Gx - Gx(m-ez) - Gz + Gz(m-ex),
+  // (K v)_z = Gy - Gy(m-ex) - Gx + Gx(m-ey) face by face (short live ranges)
+  double2 qx, qy, qz, G;
+  G = cscale(wz, csub(cadd(x00, T_(Y0, 1, 0)), cadd(T_(X0, 0, 1), y00)));          // Fz(m)
+  qx = G;
+  qy = make_double2(-G.x, -G.y);
+  G = cscale(wy, csub(cadd(z00, T_(Xp, 0, 0)), cadd(T_(Z0, 1, 0), x00)));          // Fy(m)
+  qx = csub(qx, G);
+  qz = G;
+  G = cscale(wx, csub(cadd(y00, T_(Z0, 0, 1)), cadd(T_(Yp, 0, 0), z00)));          // Fx(m)
+  qy = cadd(qy, G);
+  qz = csub(qz, G);
+  G = cscale(wz_y, csub(cadd(T_(X0, 0, -1), T_(Y0, 1, -1)), cadd(x00, T_(Y0, 0, -1))));   // Fz(m-ey)
+  qx = csub(qx, G);
+  G = cscale(wy_z, csub(cadd(T_(Zm, 0, 0), x00), cadd(T_(Zm, 1, 0), T_(Xm, 0, 0))));    // Fy(m-ez)
+  qx = cadd(qx, G);
+  G = cscale(wz_x, csub(cadd(T_(X0, -1, 0), y00), cadd(T_(X0, -1, 1), T_(Y0, -1, 0))));   // Fz(m-ex)
+  qy = cadd(qy, G);
+  G = cscale(wx_z, csub(cadd(T_(Ym, 0, 0), T_(Zm, 0, 1)), cadd(y00, T_(Zm, 0, 0))));    // Fx(m-ez)
+  qy = csub(qy, G);
+  G = cscale(wy_x, csub(cadd(T_(Z0, -1, 0), T_(Xp, -1, 0)), cadd(z00, T_(X0, -1, 0))));   // Fy(m-ex)
+  qz = csub(qz, G);
+  G = cscale(wx_y, csub(cadd(T_(Y0, 0, -1), z00), cadd(T_(Yp, 0, -1), T_(Z0, 0, -1))));   // Fx(m-ey)
+  qz = cadd(qz, G);
+#undef T_
+  E.q[0] = qx;
+  E.q[1] = qy;
+  E.q[2] = qz;
   E.kd[0] = wz + wz_y + wy + wy_z;
   E.kd[1] = wx + wx_z + wz + wz_x;
   E.kd[2] = wy + wy_x + wx + wx_y;
@@ -459,7 +463,7 @@ __global__ void __launch_bounds__(NT, 2) k_sweep(const __grid_constant__ SweepAr
       }
     }
 
-    // centre operands of step k, loaded one step ahead
+    // centre operands (mass; MODE 2: x, z) of the next step, loaded a step ahead
     auto node_of = [&](int k) { return ((long long)k * ny1 + C.j) * nx1 + C.i; };
     double mN[3];
     double2 xN[3], zN[3];
@@ -479,17 +483,6 @@ __global__ void __launch_bounds__(NT, 2) k_sweep(const __grid_constant__ SweepAr
     load_centre(kb);
 
     for (int k = kb; k < ke; ++k) {
-      double mC[3];
-      double2 xC[3], zC[3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        mC[c] = mN[c];
-        if (MODE == 2) {
-          xC[c] = xN[c];
-          zC[c] = zN[c];
-        }
-      }
-      if (k + 1 < ke) load_centre(k + 1);
       if (!kZ) wait_set(k);
       Edge3 E;
       stencil3(g, C, k, zih[k - kb + 1], zih[k - kb], zhd[k - kb],
@@ -502,22 +495,24 @@ __global__ void __launch_bounds__(NT, 2) k_sweep(const __grid_constant__ SweepAr
       for (int c = 0; c < 3; ++c) {
         if (!E.f[c]) continue;
         const long long e = vs + (long long)c * g.Nn + node;
-        const double2 q = cfma(sh, cscale(mC[c], E.p[c]), E.q[c]);   // (K + s M) v
+        const double2 q = cfma(sh, cscale(mN[c], E.p[c]), E.q[c]);   // (K + s M) v
         if (MODE == 0) {
           A.out[e] = q;
         } else if (MODE == 1) {
           A.out[e] = E.p[c];                 // p_new
           acc_c = cfma(E.p[c], q, acc_c);    // p^T A p
         } else {
-          const double2 D = make_double2(E.kd[c] + mC[c] * sh.x, mC[c] * sh.y);
-          A.x[e] = cfma(alpha, E.p[c], xC[c]);
-          const double2 zn = csub(zC[c], cmul(alpha, cdiv(q, D)));   // z - alpha D^-1 q
+          const double2 D = make_double2(E.kd[c] + mN[c] * sh.x, mN[c] * sh.y);
+          A.x[e] = cfma(alpha, E.p[c], xN[c]);
+          const double2 zn = csub(zN[c], cmul(alpha, cdiv(q, D)));   // z - alpha D^-1 q
           A.z[e] = zn;
           const double2 rn = cmul(D, zn);                           // r = D z
           acc_c = cfma(rn, zn, acc_c);
           acc_r += rn.x * rn.x + rn.y * rn.y;
         }
       }
+      // centre operands of step k+1: issued now, consumed after step k+1's stencil
+      if (k + 1 < ke) load_centre(k + 1);
       // MODE 1: set k+1's ring slots held set k-4/k-3 (no longer read): combine it now
       if (kZ && k + 1 <= ke - 1) combine(k + 1);
       __syncthreads();   // all reads of set k-2 done -> its slots may be refilled
