@@ -224,11 +224,15 @@ def run_ours(args):
 
     peak, peak_kind = _peaks()
     achieved = ALG_BYTES_PER_SUI * (sui / args.steps) / (loop_ms / args.steps * 1e-3) / 1e9
-    traffic = None
+    # measured DRAM bytes of one COCG iteration (both sweeps, all shifts active)
+    # from the committed ncu --set full capture, and the algorithmic bytes of it
+    traffic, traffic_alg = None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("bytes_per_sui")
+            tj = json.load(open(tpath))
+            traffic = tj.get("traffic_bytes_per_iteration")
+            traffic_alg = tj.get("algorithmic_bytes_per_iteration")
         except Exception:
             traffic = None
     line = {
@@ -253,6 +257,8 @@ def run_ours(args):
                    "parallelism": f"{ws} independent soundings" if ws > 1 else "1 GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
+                     "traffic_unit": "DRAM bytes per COCG iteration (k_sweep<1> + k_sweep<2>, all shifts)",
+                     "algorithmic_bytes_per_iteration": traffic_alg,
                      "kernel": "COCG sweeps k_sweep<1> + k_sweep<2>, algorithmic 128 B/SUI",
                      "peak_kind": peak_kind},
         "clocks": clk.summary(),

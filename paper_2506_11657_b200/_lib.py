@@ -42,7 +42,8 @@ SIGNATURES = {
 
 
 def lib_path() -> str:
-    return _build.LIB
+    """The in-tree library; TEM_LIB overrides it (build-variant experiments)."""
+    return os.environ.get("TEM_LIB") or _build.LIB
 
 
 def load(build_if_missing: bool = True):

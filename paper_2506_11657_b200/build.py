@@ -38,6 +38,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [nvcc_path(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
            "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O3", "-I", os.path.join(ROOT, "include"),
            "-Xptxas", "-v" if verbose else "-O3", "-o", LIB + ".tmp"] + SRC
+    extra = os.environ.get("TEM_NVCC_FLAGS", "").split()
+    cmd = cmd[:-len(SRC) - 2] + extra + cmd[-len(SRC) - 2:]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)

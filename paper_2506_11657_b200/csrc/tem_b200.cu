@@ -237,6 +237,7 @@ struct tem_ctx {
   size_t e2e_bytes = 0;
   // stats of the last solve
   tem_solve_stats stats{};
+  int sweep_per_sm = 2;             // resident sweep CTAs per SM (occupancy of k_sweep<1>)
 };
 
 static int check_S(int S) {
@@ -256,7 +257,7 @@ static void sweep_geometry(const tem_ctx* c, int S, int nslot, tem::SweepArgs& A
   A.nslot = nslot;
   A.ntx = (c->g.n[0] + tem::TX - 1) / tem::TX;
   A.nty = (c->g.n[1] + tem::TY - 1) / tem::TY;
-  const int target = 4 * c->num_sms * 2;
+  const int target = 4 * c->num_sms * c->sweep_per_sm;
   const int base = A.ntx * A.nty * nslot;
   int nzc = 1;
   while (base * nzc < target && c->g.n[2] / (nzc * 2) >= 16) nzc *= 2;
@@ -379,6 +380,11 @@ int tem_create(int nx, int ny, int nz, const double* hx, const double* hy, const
   if (int rc = sweep_attrs()) {
     tem_destroy(c);
     return rc;
+  }
+  {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tem::k_sweep<1>, tem::NT, tem::kSmemDirap);
+    c->sweep_per_sm = std::max(1, per_sm);
   }
   *out = c;
   return TEM_OK;

@@ -29,7 +29,11 @@
 namespace tem {
 
 constexpr int TX = 32;                    // tile nodes along x (one warp row)
-constexpr int TY = 8;                     // tile nodes along y
+#ifndef TEM_TY
+#define TEM_TY 8
+#endif
+constexpr int TY = TEM_TY;                // tile nodes along y (8: 2 CTAs/SM; 16: 1 CTA/SM)
+constexpr int kMinBlocks = TY <= 8 ? 2 : 1;
 constexpr int NT = TX * TY;               // threads per CTA
 constexpr int HX = TX + 2, HY = TY + 2;   // halo-extended tile
 constexpr int TILE_BYTES = HX * HY * 16;  // one plane tile as delivered by TMA (5440 B)
@@ -38,8 +42,8 @@ constexpr int TS2 = TILE_STRIDE / 16;     // slot pitch in double2
 
 // ring: sets q = {X(q+1), Y(q+1), Z(q)}; X,Y: 5 slots, Z: 4 slots (+ MODE 1 z staging 2 x 3)
 constexpr int R_XY = 5, R_Z = 4;
-constexpr size_t kSmemDirect = 128 + (size_t)(2 * R_XY + R_Z) * TILE_STRIDE;        // 77 KB
-constexpr size_t kSmemDirap = kSmemDirect + (size_t)6 * TILE_STRIDE;              // 110 KB
+constexpr size_t kSmemDirect = 128 + (size_t)(2 * R_XY + R_Z) * TILE_STRIDE;        // 77 KB at TY=8
+constexpr size_t kSmemDirap = kSmemDirect + (size_t)6 * TILE_STRIDE;              // 110 KB at TY=8
 constexpr int kMaxChunk = 128;            // max planes per z-chunk (z tables in smem)
 
 struct ShiftState {
@@ -350,7 +354,7 @@ __device__ __forceinline__ void block_coords(const SweepArgs& A, int& a, int& tx
 // p_new = z + beta p_old (at the end of step q-1, two sets ahead), so MODE 1
 // needs 20 tiles (110 KB) and also runs 2 CTAs per SM.
 template <int MODE>
-__global__ void __launch_bounds__(NT, 2) k_sweep(const __grid_constant__ SweepArgs A,
+__global__ void __launch_bounds__(NT, kMinBlocks) k_sweep(const __grid_constant__ SweepArgs A,
                                                  const __grid_constant__ CUtensorMap tmv,
                                                  const __grid_constant__ CUtensorMap tmz) {
   constexpr bool kZ = (MODE == 1);
