@@ -262,7 +262,6 @@ static void sweep_geometry(const tem_ctx* c, int S, int nslot, tem::SweepArgs& A
   int nzc = 1;
   while (base * nzc < target && c->g.n[2] / (nzc * 2) >= 16) nzc *= 2;
   if (const char* env = getenv("TEM_FORCE_NZC")) nzc = std::max(1, atoi(env));  // tests
-  A.yfirst = getenv("TEM_YFIRST") ? atoi(getenv("TEM_YFIRST")) : 0;             // experiments
   nzc = std::max(nzc, (c->g.n[2] + tem::kMaxChunk - 1) / tem::kMaxChunk);
   A.kchunk = (c->g.n[2] + nzc - 1) / nzc;
   A.nzc = (c->g.n[2] + A.kchunk - 1) / A.kchunk;
