@@ -83,3 +83,18 @@ def test_synthesis_sampled_rows(name):
     assert np.all(np.abs(ur - uo) <= 1e-14 * T + 1e-300)
     # the channels carry signal: the earliest channel is not a cancellation to zero
     assert np.linalg.norm(uo[:, 0]) > 1e-6 * np.linalg.norm(T[:, 0])
+
+
+def test_bench_config_deterministic_and_synthesis_consistent():
+    """Two solves of the bench workload in bench's configuration give
+    bit-identical iterates and iteration counts (fixed-order reductions)."""
+    wl = make_workload("hetero")
+    table = RationalTable.load("hetero")
+    fw = TemForward(wl.grid.hx, wl.grid.hy, wl.grid.hz)
+    sigma = torch.from_numpy(fw.sigma_layout(wl.sigma)).cuda()
+    f = torch.from_numpy(fw.source_vector(wl.source)).cuda()
+    mass = fw.edge_mass(sigma)
+    x1, i1, _ = fw.cocg(mass, f, table.shifts)
+    x2, i2, _ = fw.cocg(mass, f, table.shifts)
+    assert np.array_equal(i1, i2)
+    assert torch.equal(x1, x2)
