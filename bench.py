@@ -132,6 +132,16 @@ def _workload_for_rank(name: str, rank: int):
     return wl
 
 
+def _poles(args, wl):
+    """Shifts/residues: the committed table (data/rational, the inputs the
+    parity tests share with the oracle) or the library's own host fit
+    (tem_fit_family) for the workload's channels and degree."""
+    from paper_2506_11657_b200 import RationalTable
+    if args.poles == "fit":
+        return RationalTable.fit(wl.times, wl.n_poles)
+    return RationalTable.load(args.config)
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -147,7 +157,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
 
     wl = _workload_for_rank(args.config, rank)
-    table = RationalTable.load(args.config)
+    table = _poles(args, wl)
     fw = TemForward(wl.grid.hx, wl.grid.hy, wl.grid.hz, device=dev)
     sigma = torch.from_numpy(fw.sigma_layout(wl.sigma)).to(dev)
     f = torch.from_numpy(fw.source_vector(wl.source)).to(dev)
@@ -249,6 +259,7 @@ def run_ours(args):
         "dtype": "c128",
         "data": "synthetic (seeded earth model, BASELINE configs[4] shape)",
         "config": {"workload": args.config, "unknowns": N, "shifts": S, "channels": K,
+                   "poles": args.poles, "uniform_error": table.uniform_error,
                    "degree": int(2 * table.is_pair.sum() + (~table.is_pair).sum()),
                    "tol": args.tol, "iterations_max": int(st["iterations"]),
                    "iterations_per_shift": [int(i) for i in iters],
@@ -331,6 +342,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="large")
     ap.add_argument("--tol", type=float, default=1e-10)
+    ap.add_argument("--poles", default="fit", choices=["table", "fit"])
     ap.add_argument("--maxit", type=int, default=200000)
     ap.add_argument("--cpu-iters", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")

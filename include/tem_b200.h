@@ -145,6 +145,22 @@ int tem_forward_host(tem_ctx* ctx, const double* sigma, const double* f, int S,
                      const int* is_pair, double tol, int maxit, double* u,
                      int* iters, double* relres);
 
+/* Host-side construction of the shared-pole family, computed once before the
+ * solves (§3.2 eq:ratfam, RKFIT objective eq:rkfit with a diagonal
+ * surrogate of dense eigenvalues on [0, inf) and v = 1; R3-R5).
+ *   K, t:       HOST double[K], time channels in seconds (> 0)
+ *   w:          HOST double[K] weights w_j of eq:rkfit, or NULL for unit weights
+ *   m:          degree m-hat (2..64); iters: relocation sweeps (<= 0: 12)
+ * Outputs (HOST, caller-allocated for the worst case n_rep = m):
+ *   n_rep:      number of shifted systems (one per conjugate pair + one per real pole)
+ *   shifts:     complex[m]: s_i = -xi_i / t_max (1/s), the shifts of tem_cocg_solve
+ *   residues:   complex[m][K]: alpha_ij / t_max, row i = representative pole i
+ *   is_pair:    int[m]: 1 if pole i stands for a conjugate pair (weight 2 in eq:rmj)
+ *   uniform_error: (may be NULL) eq:uniform_error estimated on a log grid.
+ * Deterministic; CPU only; TEM_EINVAL on bad arguments. */
+int tem_fit_family(int K, const double* t, const double* w, int m, int iters, int* n_rep,
+                   double* shifts, double* residues, int* is_pair, double* uniform_error);
+
 #ifdef __cplusplus
 }
 #endif

@@ -13,7 +13,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = [os.path.join(HERE, "csrc", "tem_b200.cu")]
+SRC = [os.path.join(HERE, "csrc", "tem_b200.cu"), os.path.join(HERE, "csrc", "tem_rkfit.cpp")]
 DEPS = sorted(glob.glob(os.path.join(HERE, "csrc", "*"))) + [os.path.join(ROOT, "include", "tem_b200.h")]
 LIB = os.path.join(HERE, "libtem_b200.so")
 

@@ -216,6 +216,8 @@ __global__ void k_synth(Grid g, int S, int K, const double2* __restrict__ res,
 
 }  // namespace
 
+void tem_set_error(const std::string& msg) { g_last_error = msg; }
+
 // ====================================================================== C ABI
 
 struct tem_ctx {

@@ -66,6 +66,28 @@ class RationalTable:
         return self.shifts.size
 
     @classmethod
+    def fit(cls, times, degree: int, weights=None, iters: int = 12) -> "RationalTable":
+        """Shared-pole family for these time channels, computed by the
+        library's host-side fit (tem_fit_family; §3.2 eq:ratfam /
+        eq:rkfit).  CPU only, once per channel set."""
+        lib = _lib.load()
+        t = np.ascontiguousarray(times, dtype=np.float64)
+        K, m = t.size, int(degree)
+        w = None if weights is None else np.ascontiguousarray(weights, dtype=np.float64)
+        n_rep = ctypes.c_int()
+        sh = np.zeros(2 * m)
+        res = np.zeros(2 * m * K)
+        ip = np.zeros(m, dtype=np.int32)
+        ue = ctypes.c_double()
+        _lib.check(lib.tem_fit_family(K, _dptr(t), None if w is None else _dptr(w), m, int(iters),
+                                      ctypes.byref(n_rep), _dptr(sh), _dptr(res), _iptr(ip),
+                                      ctypes.byref(ue)))
+        n = n_rep.value
+        shifts = sh.view(np.complex128)[:n].copy()
+        residues = res.view(np.complex128).reshape(m, K)[:n].copy()
+        return cls(shifts, residues, ip[:n].astype(bool), t, ue.value)
+
+    @classmethod
     def load(cls, name_or_path: str) -> "RationalTable":
         """Read data/rational/<name>.json (inputs computed once on the host
         by scripts/make_rational_tables.py)."""

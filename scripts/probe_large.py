@@ -7,7 +7,8 @@ from paper_2506_11657_b200 import RationalTable, TemForward
 from workloads import make_workload
 name = sys.argv[1] if len(sys.argv) > 1 else "large"
 budget = int(sys.argv[2]) if len(sys.argv) > 2 else 2000
-wl = make_workload(name); table = RationalTable.load(name)
+wl = make_workload(name)
+table = RationalTable.fit(wl.times, wl.n_poles) if os.environ.get("POLES") == "fit" else RationalTable.load(name)
 fw = TemForward(wl.grid.hx, wl.grid.hy, wl.grid.hz)
 sigma = torch.from_numpy(fw.sigma_layout(wl.sigma)).cuda()
 f = torch.from_numpy(fw.source_vector(wl.source)).cuda()

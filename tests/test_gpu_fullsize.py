@@ -98,3 +98,21 @@ def test_bench_config_deterministic_and_synthesis_consistent():
     x2, i2, _ = fw.cocg(mass, f, table.shifts)
     assert np.array_equal(i1, i2)
     assert torch.equal(x1, x2)
+
+
+def test_bench_default_poles_true_residual():
+    """bench.py's default inputs: the library's own host fit (tem_fit_family)
+    for the 14M config; every shift's true residual via the oracle CSR."""
+    wl = make_workload("large")
+    table = RationalTable.fit(wl.times, wl.n_poles)
+    assert table.uniform_error < 1e-3
+    fw = TemForward(wl.grid.hx, wl.grid.hy, wl.grid.hz)
+    sigma = torch.from_numpy(fw.sigma_layout(wl.sigma)).cuda()
+    f = torch.from_numpy(fw.source_vector(wl.source)).cuda()
+    mass = fw.edge_mass(sigma)
+    x, iters, relres = fw.cocg(mass, f, table.shifts, tol=1e-10, maxit=200000)
+    assert np.all(relres <= 1e-10)
+    asm = yee.assemble(wl)
+    slots = fw.slot(*asm.keys())
+    for i, s in enumerate(table.shifts):
+        assert ofw.relative_residual(asm, s, x[i].cpu().numpy()[slots]) <= 5e-10

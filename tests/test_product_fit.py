@@ -1,0 +1,88 @@
+"""CPU tests of the library's host-side shared-pole fit (tem_fit_family,
+paper_2506_11657_b200/csrc/tem_rkfit.cpp), pinned to PAPER.md Table 1 and
+cross-checked against the independent oracle fit (oracle/rkfit.py)."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import rkfit
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def RationalTable():
+    from paper_2506_11657_b200 import build
+    build.build()
+    from paper_2506_11657_b200.solver import RationalTable
+    return RationalTable
+
+
+def _table1():
+    rows = {}
+    with open(os.path.join(GOLDEN, "table1.csv")) as fh:
+        lines = [ln.strip() for ln in fh if ln.strip() and not ln.startswith("#")]
+    header = lines[0].split(",")
+    ratios = {"r1": 1.0, "r1e1": 1e1, "r1e2": 1e2, "r1e3": 1e3, "r1e4": 1e4, "r1e5": 1e5}
+    for ln in lines[1:]:
+        parts = ln.split(",")
+        if parts[0] != "avgKstar":
+            for col, val in zip(header[1:], parts[1:]):
+                rows[(ratios[col], float(parts[0]))] = int(val)
+    return rows
+
+
+TABLE1 = _table1()
+
+
+def _eval(tab, j, x):
+    """u_j(x) = sum_i w_i Re(alpha_ij / (x + s_i)) in the physical variable."""
+    w = np.where(tab.is_pair, 2.0, 1.0)
+    return np.sum(w[:, None] * (tab.residues[:, j][:, None] / (x[None, :] + tab.shifts[:, None])).real,
+                  axis=0)
+
+
+@pytest.mark.parametrize("ratio,acc", [(1e1, 1e-4), (1e3, 1e-6), (1e4, 1e-4), (1e5, 1e-2)])
+def test_table1_two_sided(RationalTable, ratio, acc):
+    deg = TABLE1[(ratio, acc)]
+    m = deg + deg % 2
+    t = np.logspace(-np.log10(ratio), 0.0, 31)
+    assert RationalTable.fit(t, m).uniform_error <= acc
+    assert RationalTable.fit(t, m - 4).uniform_error > acc
+
+
+def test_independent_error_check_and_oracle_agreement(RationalTable):
+    """The library's reported error is re-measured here on a different grid
+    (physical variable), and is within 2x of the oracle fit's."""
+    t = np.logspace(-5, -2, 31)
+    tab = RationalTable.fit(t, 16)
+    x = np.concatenate([[0.0], np.logspace(-2, 9, 5000)])
+    err = max(np.max(np.abs(_eval(tab, j, x) - np.exp(-t[j] * x))) for j in range(t.size))
+    assert err <= 1.05 * tab.uniform_error
+    assert err >= 0.5 * tab.uniform_error
+    fam = rkfit.fit_family(t, 16)
+    assert tab.uniform_error <= 2.0 * rkfit.uniform_error(fam)
+    # 8 conjugate pairs, all shifts off (-inf, 0] (poles off [0, inf))
+    assert tab.n_shift == 8 and np.all(tab.is_pair)
+    assert np.all(np.abs(tab.shifts.imag) > 0) or np.all(tab.shifts.real > 0)
+
+
+def test_weights_and_degenerate_inputs(RationalTable):
+    from paper_2506_11657_b200 import _lib
+    t = np.logspace(-3, 0, 11)
+    a = RationalTable.fit(t, 12)
+    b = RationalTable.fit(t, 12, weights=np.ones(11))
+    np.testing.assert_array_equal(a.shifts, b.shifts)      # NULL weights == unit weights
+    with pytest.raises(_lib.TemError):
+        RationalTable.fit(t, 1)
+    with pytest.raises(_lib.TemError):
+        RationalTable.fit(np.array([1e-3, -1.0]), 8)
+
+
+def test_single_channel_decays_and_is_real(RationalTable):
+    t = np.array([1e-3])
+    tab = RationalTable.fit(t, 10)
+    x = np.logspace(2, 12, 50)
+    u = _eval(tab, 0, x)
+    assert abs(u[-1]) < 1e-6 and abs(_eval(tab, 0, np.array([0.0]))[0] - 1.0) < tab.uniform_error * 1.01
