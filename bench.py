@@ -35,7 +35,15 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-ALG_BYTES_PER_SUI = 128  # x, r, p streamed at the 2-sweep COCG minimum
+# algorithmic HBM bytes per shift-unknown-iteration of each
+# COCG scheme (complex fp64, 16 B per value):
+#   two_sweep: sweep 1 reads z, p_old, writes p (48); sweep 2 reads p, x, z,
+#              writes x, z (80)                                       -> 128
+#   split:     pass 1 reads z, p_old, writes p, z (64) and, every second
+#              iteration, reads and writes x (+32); pass 2 reads z (16) -> 96
+ALG_BYTES_PER_SUI = {"two_sweep": 128, "split": 96}
+KERNELS = {"two_sweep": "COCG sweeps k_sweep<1> + k_sweep<2>",
+           "split": "split COCG passes k_sweep<3>/<4> (pass 1) + k_delta (pass 2)"}
 
 
 def _peaks():
@@ -159,6 +167,9 @@ def run_ours(args):
     wl = _workload_for_rank(args.config, rank)
     table = _poles(args, wl)
     fw = TemForward(wl.grid.hx, wl.grid.hy, wl.grid.hz, device=dev)
+    if args.solver:
+        fw.solver = args.solver
+    solver = fw.solver
     sigma = torch.from_numpy(fw.sigma_layout(wl.sigma)).to(dev)
     f = torch.from_numpy(fw.source_vector(wl.source)).to(dev)
     S, K = table.residues.shape
@@ -233,14 +244,14 @@ def run_ours(args):
         return None
 
     peak, peak_kind = _peaks()
-    achieved = ALG_BYTES_PER_SUI * (sui / args.steps) / (loop_ms / args.steps * 1e-3) / 1e9
+    achieved = ALG_BYTES_PER_SUI[solver] * (sui / args.steps) / (loop_ms / args.steps * 1e-3) / 1e9
     # measured DRAM bytes of one COCG iteration (both sweeps, all shifts active)
     # from the committed ncu --set full capture, and the algorithmic bytes of it
     traffic, traffic_alg = None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            tj = json.load(open(tpath))
+            tj = json.load(open(tpath)).get(solver, {})
             traffic = tj.get("traffic_bytes_per_iteration")
             traffic_alg = tj.get("algorithmic_bytes_per_iteration")
         except Exception:
@@ -268,10 +279,11 @@ def run_ours(args):
                    "parallelism": f"{ws} independent soundings" if ws > 1 else "1 GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "traffic_unit": "DRAM bytes per COCG iteration (k_sweep<1> + k_sweep<2>, all shifts)",
+                     "traffic_unit": "DRAM bytes per COCG iteration (all sweeps, all shifts active; "
+                                     "split: mean of an even and an odd iteration)",
                      "algorithmic_bytes_per_iteration": traffic_alg,
-                     "kernel": "COCG sweeps k_sweep<1> + k_sweep<2>, algorithmic 128 B/SUI",
-                     "peak_kind": peak_kind},
+                     "kernel": f"{KERNELS[solver]}, algorithmic {ALG_BYTES_PER_SUI[solver]} B/SUI",
+                     "solver": solver, "peak_kind": peak_kind},
         "clocks": clk.summary(),
         "e2e": e2e,
         "gpu_launches": launches,
@@ -345,6 +357,8 @@ def main():
     ap.add_argument("--poles", default="fit", choices=["table", "fit"])
     ap.add_argument("--maxit", type=int, default=200000)
     ap.add_argument("--cpu-iters", type=int, default=8)
+    ap.add_argument("--solver", default=None, choices=["split", "two_sweep"],
+                    help="COCG scheme (default: the library's, tem_get_solver)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -118,6 +118,23 @@ int tem_cocg_solve(tem_ctx* ctx, const double* mass, const double* f, int S,
                    void* work, size_t work_bytes, int* iters, double* relres,
                    void* stream);
 
+/* Iteration scheme of tem_cocg_solve.  Both are Jacobi-COCG: the same Krylov
+ * iterates in exact arithmetic, the same stopping rule, the same outputs.
+ *   TEM_SOLVER_SPLIT (default): COCG with the inner product p^T A p of the
+ *     step length expanded into three inner products of the previous
+ *     iteration (Chronopoulos-Gear arrangement, exact expansion: DESIGN.md
+ *     reading R10), so each iteration is ONE full update sweep (p, z and,
+ *     every second iteration, x) plus one read-only sweep for z^T A z:
+ *     96 B per unknown per shift per iteration.
+ *   TEM_SOLVER_TWO_SWEEP: the textbook recursion, alpha = r^T z / p^T A p;
+ *     128 B per unknown per shift per iteration.
+ * tem_set_solver returns TEM_EINVAL for any other value; tem_get_solver
+ * returns the current scheme (TEM_EINVAL for a NULL context). */
+#define TEM_SOLVER_SPLIT 0
+#define TEM_SOLVER_TWO_SWEEP 1
+int tem_set_solver(tem_ctx* ctx, int solver);
+int tem_get_solver(const tem_ctx* ctx);
+
 /* Statistics of the last tem_cocg_solve on this context. */
 typedef struct {
   double loop_ms;             /* GPU time (CUDA events) of init + iteration loop */

@@ -35,6 +35,8 @@ SIGNATURES = {
     "tem_cocg_solve": ([_P, _P, _P, ctypes.c_int, _D, ctypes.c_double, ctypes.c_int, _P, _P,
                         ctypes.c_size_t, _I, _D, _P], ctypes.c_int),
     "tem_last_solve_stats": ([_P, ctypes.POINTER(SolveStats)], ctypes.c_int),
+    "tem_set_solver": ([_P, ctypes.c_int], ctypes.c_int),
+    "tem_get_solver": ([_P], ctypes.c_int),
     "tem_synthesize": ([_P, ctypes.c_int, ctypes.c_int, _D, _I, _P, _P, _P], ctypes.c_int),
     "tem_forward_host": ([_P, _D, _D, ctypes.c_int, _D, ctypes.c_int, _D, _I, ctypes.c_double,
                           ctypes.c_int, _D, _I, _D], ctypes.c_int),

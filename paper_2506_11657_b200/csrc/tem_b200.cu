@@ -100,7 +100,7 @@ __device__ __forceinline__ double kdiag(const Grid& g, int a, const int pos[3]) 
 
 // COCG init (z-form): x = 0, p0 = p1 = 0, z = D^-1 f; rho = f^T z, ||f||^2.
 // Block b serves shift b % S.
-__global__ void __launch_bounds__(256) k_init(tem::SweepArgs A, double2* p0, double2* p1,
+__global__ void __launch_bounds__(256) k_init(tem::SweepArgs A, double2* p0, double2* p1, double2* z1,
                                               const double* __restrict__ f) {
   __shared__ double red[3 * 8];
   const Grid& g = A.g;
@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(256) k_init(tem::SweepArgs A, double2* p0, dou
     A.z[vs + slot] = zv;
     p0[vs + slot] = tem::czero();
     p1[vs + slot] = tem::czero();
+    if (z1) z1[vs + slot] = tem::czero();
   }
   tem::block_sum_n<256>(rho, rr, red);
   if (threadIdx.x == 0) {
@@ -168,6 +169,22 @@ __global__ void __launch_bounds__(256) k_init(tem::SweepArgs A, double2* p0, dou
     A.ctl->n_active = na;
     A.ctl->ticket[0] = 0;
   }
+}
+
+// Split solver epilogue: a shift whose last iteration i was even (iters odd)
+// has x_i in x (x advances every second iteration); x_{i+1} = x_i + alpha_i p_i
+// with p_i in p1.  alpha_i is `alpha` if the shift stopped, `alpha_prev` if it
+// is still running (maxit reached).  Block b serves shift b % S.
+__global__ void __launch_bounds__(256) k_xfix(tem::SweepArgs A, const double2* __restrict__ p1) {
+  const int S = A.S;
+  const int s = blockIdx.x % S;
+  const tem::ShiftState& st = A.st[s];
+  if ((st.iters & 1) == 0) return;
+  const double2 a = st.active ? st.alpha_prev : st.alpha;
+  const long long vs = (long long)s * 3 * A.g.Nn;
+  const int nb = gridDim.x / S;
+  for (long long slot = (blockIdx.x / S) * 256LL + threadIdx.x; slot < 3 * A.g.Nn; slot += (long long)nb * 256)
+    A.x[vs + slot] = tem::cfma(a, p1[vs + slot], A.x[vs + slot]);
 }
 
 // u[k][slot] = sum_s w_s Re(res[k][s] x[s][slot]); 0 on non-free slots.
@@ -240,6 +257,7 @@ struct tem_ctx {
   // stats of the last solve
   tem_solve_stats stats{};
   int sweep_per_sm = 2;             // resident sweep CTAs per SM (occupancy of k_sweep<1>)
+  int solver = TEM_SOLVER_SPLIT;
 };
 
 static int check_S(int S) {
@@ -287,13 +305,18 @@ static int sweep_attrs() {
   TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmemDirect));
   TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmemDirect));
   TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmemDirap));
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmemDirap));
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmemDirap));
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_delta<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmemDelta));
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_delta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmemDelta));
   done = true;
   return TEM_OK;
 }
 
 // 5-D tiled tensor map over a shift block [S][3][nz+1][ny+1][nx+1] complex
 // fp64 (as 2(nx+1) doubles innermost); box = one halo-extended plane tile.
-static int make_tmap(const tem_ctx* c, int S, const void* base, CUtensorMap* tm) {
+static int make_tmap(const tem_ctx* c, int S, const void* base, CUtensorMap* tm,
+                     int box_x = tem::HX, int box_y = tem::HY) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -306,7 +329,7 @@ static int make_tmap(const tem_ctx* c, int S, const void* base, CUtensorMap* tm)
   const cuuint64_t nx1 = c->g.n[0] + 1, ny1 = c->g.n[1] + 1, nz1 = c->g.n[2] + 1;
   const cuuint64_t dims[5] = {2 * nx1, ny1, nz1, 3, (cuuint64_t)S};
   const cuuint64_t strides[4] = {16 * nx1, 16 * nx1 * ny1, 16 * nx1 * ny1 * nz1, 48 * nx1 * ny1 * nz1};
-  const cuuint32_t box[5] = {2 * tem::HX, tem::HY, 1, 1, 1};
+  const cuuint32_t box[5] = {2 * (cuuint32_t)box_x, (cuuint32_t)box_y, 1, 1, 1};
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   if (const char* env = getenv("TEM_L2PROMO")) {  // experiments
@@ -440,21 +463,26 @@ int tem_apply_shifted(tem_ctx* c, const double* mass, int S, const double* shift
 }
 
 struct WorkLayout {
-  size_t z, p0, p1, st, ctl, part_c, part_r, total;
+  size_t z, z1, p0, p1, st, ctl, part_c, part_r, part9, total;
+  size_t nparts;
 };
 
 static WorkLayout work_layout(const tem_ctx* c, int S) {
   WorkLayout L{};
   const size_t vec = (size_t)3 * c->g.Nn * S * sizeof(double2);
   const size_t nparts = (size_t)std::max(max_sweep_grid(c, S), 1024 * S);
+
   size_t o = 0;
   L.z = o;      o = align_up(o + vec, 256);
+  L.z1 = o;     o = align_up(o + vec, 256);
   L.p0 = o;     o = align_up(o + vec, 256);
   L.p1 = o;     o = align_up(o + vec, 256);
   L.st = o;     o = align_up(o + sizeof(tem::ShiftState) * TEM_MAX_SHIFTS, 256);
   L.ctl = o;    o = align_up(o + sizeof(tem::Control), 256);
   L.part_c = o; o = align_up(o + nparts * sizeof(double2), 256);
   L.part_r = o; o = align_up(o + nparts * sizeof(double), 256);
+  L.part9 = o;  o = align_up(o + tem::kSplitPart * nparts * sizeof(double), 256);
+  L.nparts = nparts;
   L.total = o;
   return L;
 }
@@ -463,6 +491,14 @@ size_t tem_cocg_workspace_bytes(const tem_ctx* c, int S) {
   if (!c || S < 1 || S > TEM_MAX_SHIFTS) return 0;
   return work_layout(c, S).total;
 }
+
+static int finish_solve(tem_ctx* c, int S, std::vector<tem::ShiftState>& st, const tem::ShiftState* dev_st,
+                        cudaEvent_t ev0, cudaEvent_t ev1, cudaStream_t stream, long long launches, int grid,
+                        int block, int* iters, double* relres);
+
+static int solve_split(tem_ctx* c, const double* mass, const double* f, int S, const double* shifts,
+                       double tol, int maxit, double* x, char* w, const WorkLayout& L, int* iters,
+                       double* relres, cudaStream_t stream);
 
 int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const double* shifts,
                    double tol, int maxit, double* x, void* work, size_t work_bytes, int* iters,
@@ -473,6 +509,10 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
   const WorkLayout L = work_layout(c, S);
   if (work_bytes < L.total) return fail(TEM_EINVAL, "tem_cocg_solve: workspace too small");
   cudaStream_t stream = (cudaStream_t)stream_;
+  if (c->solver == TEM_SOLVER_SPLIT)
+    return solve_split(c, mass, f, S, shifts, tol, maxit, x, static_cast<char*>(work), L, iters, relres,
+                       stream);
+
   char* w = static_cast<char*>(work);
 
   tem::SweepArgs base{};
@@ -556,7 +596,7 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
   TEM_CUDA(cudaEventCreate(&ev1));
   TEM_CUDA(cudaEventRecord(ev0, stream));
   const int init_grid = S * std::max(1, std::min(64, (int)((3 * c->g.Nn + 255) / 256)));
-  k_init<<<init_grid, 256, 0, stream>>>(base, P[0], P[1], f);
+  k_init<<<init_grid, 256, 0, stream>>>(base, P[0], P[1], nullptr, f);
   TEM_CUDA(cudaGetLastError());
   long long launches = 1;
 
@@ -596,7 +636,13 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
     }
   }
   TEM_CUDA(cudaEventRecord(ev1, stream));
-  TEM_CUDA(cudaMemcpyAsync(st.data(), base.st, sizeof(tem::ShiftState) * S, cudaMemcpyDeviceToHost, stream));
+  return finish_solve(c, S, st, base.st, ev0, ev1, stream, launches, grid, tem::NT, iters, relres);
+}
+
+static int finish_solve(tem_ctx* c, int S, std::vector<tem::ShiftState>& st, const tem::ShiftState* dev_st,
+                        cudaEvent_t ev0, cudaEvent_t ev1, cudaStream_t stream, long long launches, int grid,
+                        int block, int* iters, double* relres) {
+  TEM_CUDA(cudaMemcpyAsync(st.data(), dev_st, sizeof(tem::ShiftState) * S, cudaMemcpyDeviceToHost, stream));
   TEM_CUDA(cudaStreamSynchronize(stream));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ev0, ev1);
@@ -619,11 +665,175 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
   c->stats.shift_iterations = shift_iters;
   c->stats.iterations = max_it;
   c->stats.grid = grid;   // with all shifts active
-  c->stats.block = tem::NT;
+  c->stats.block = block;
   if (status == TEM_EBREAKDOWN) return fail(status, "tem_cocg_solve: COCG breakdown");
   if (status == TEM_ENOCONV) return fail(status, "tem_cocg_solve: not converged within maxit");
   return TEM_OK;
 }
+
+// Split COCG (tem_sweep.cuh MODE 3/4 + k_delta): per iteration i
+//   pass 1 (k_sweep<3> for even i, <4> for odd i): p_i = z_i + beta p_{i-1},
+//     z_{i+1} = z_i - alpha_i D^-1 A p_i, odd i also x_{i+1} = x_{i-1} +
+//     alpha_{i-1} p_{i-1} + alpha_i p_i; partials gamma, eps, mu, ||r||^2
+//   pass 2 (k_delta): delta = z_{i+1}^T A z_{i+1} by faces; the last CTA
+//     forms alpha_{i+1}, beta_{i+1} and the active list (finalize_split).
+// z and p ping-pong: pass 1 with parity q = i & 1 reads Z[q], P[q] and writes
+// Z[1-q], P[1-q]; pass 2 reads Z[1-q].  Start: k_init, then k_delta<true> on z_0
+// (alpha_0 = gamma_0 / delta_0).  End: k_xfix for shifts whose x lags.
+static int solve_split(tem_ctx* c, const double* mass, const double* f, int S, const double* shifts,
+                       double tol, int maxit, double* x, char* w, const WorkLayout& L, int* iters,
+                       double* relres, cudaStream_t stream) {
+  double2* Z[2] = {reinterpret_cast<double2*>(w + L.z), reinterpret_cast<double2*>(w + L.z1)};
+  double2* P[2] = {reinterpret_cast<double2*>(w + L.p0), reinterpret_cast<double2*>(w + L.p1)};
+  CUtensorMap tmZ[2], tmP[2];
+  for (int q = 0; q < 2; ++q) {
+    if (int rc = make_tmap(c, S, Z[q], &tmZ[q])) return rc;
+    if (int rc = make_tmap(c, S, P[q], &tmP[q])) return rc;
+  }
+  tem::SweepArgs base{};
+  int grid = 0;
+  sweep_geometry(c, S, S, base, &grid);
+  base.mass = mass;
+  base.x = reinterpret_cast<double2*>(x);
+  base.st = reinterpret_cast<tem::ShiftState*>(w + L.st);
+  base.ctl = reinterpret_cast<tem::Control*>(w + L.ctl);
+  base.part_c = reinterpret_cast<double2*>(w + L.part_c);
+  base.part_r = reinterpret_cast<double*>(w + L.part_r);
+  base.part = reinterpret_cast<double*>(w + L.part9);
+  base.pstride = (int)L.nparts;
+  if (const char* env = getenv("TEM_XDIRECT")) base.force_xdirect = atoi(env);   // tests
+
+  struct Cfg {
+    tem::SweepArgs a1[2], a2[2];
+    int grid;
+  };
+  auto make_cfg = [&](int nslot) {
+    Cfg k{};
+    tem::SweepArgs g0 = base;
+    sweep_geometry(c, S, nslot, g0, &k.grid);
+    for (int q = 0; q < 2; ++q) {
+      k.a1[q] = g0;
+      k.a1[q].zin = Z[q];
+      k.a1[q].z = Z[1 - q];
+      k.a1[q].out = P[1 - q];
+      k.a1[q].pold = P[q];
+      k.a2[q] = g0;
+    }
+    return k;
+  };
+  const size_t smem1 = tem::kSmemDirap, smem2 = tem::kSmemDelta;
+  auto launch_iter = [&](const Cfg& k, int q, cudaStream_t st_) {
+    if (q == 0)
+      tem::k_sweep<3><<<k.grid, tem::NT, smem1, st_>>>(k.a1[0], tmP[0], tmZ[0]);
+    else
+      tem::k_sweep<4><<<k.grid, tem::NT, smem1, st_>>>(k.a1[1], tmP[1], tmZ[1]);
+    tem::k_delta<false><<<k.grid, tem::NT, smem2, st_>>>(k.a2[q], tmZ[1 - q]);
+  };
+  const std::vector<const void*> key = {mass, x, w, f, (const void*)2};
+  if (c->graph_key != key || c->graph_S != S) {
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    c->graphs.clear();
+    c->graph_key = key;
+    c->graph_S = S;
+  }
+  auto get_graph = [&](const Cfg& k, int nslot, cudaGraphExec_t* out) -> int {
+    const long long id = (long long)nslot * 4096 + k.a1[0].nzc;
+    auto it = c->graphs.find(id);
+    if (it != c->graphs.end()) {
+      *out = it->second;
+      return TEM_OK;
+    }
+    cudaGraph_t gr;
+    TEM_CUDA(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < kChunk; ++i) launch_iter(k, i & 1, c->cap_stream);
+    TEM_CUDA(cudaStreamEndCapture(c->cap_stream, &gr));
+    cudaGraphExec_t ex;
+    cudaError_t e = cudaGraphInstantiate(&ex, gr, 0);
+    cudaGraphDestroy(gr);
+    if (e != cudaSuccess) return fail(TEM_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    c->graphs[id] = ex;
+    *out = ex;
+    return TEM_OK;
+  };
+
+  std::vector<tem::ShiftState> st(S);
+  for (int s = 0; s < S; ++s) {
+    memset(&st[s], 0, sizeof(tem::ShiftState));
+    st[s].s = make_double2(shifts[2 * s], shifts[2 * s + 1]);
+  }
+  tem::Control ctl{};
+  ctl.tol = tol;
+  TEM_CUDA(cudaMemcpyAsync(base.st, st.data(), sizeof(tem::ShiftState) * S, cudaMemcpyHostToDevice, stream));
+  TEM_CUDA(cudaMemcpyAsync(base.ctl, &ctl, sizeof(tem::Control), cudaMemcpyHostToDevice, stream));
+
+  cudaEvent_t ev0, ev1;
+  TEM_CUDA(cudaEventCreate(&ev0));
+  TEM_CUDA(cudaEventCreate(&ev1));
+  TEM_CUDA(cudaEventRecord(ev0, stream));
+  {
+    tem::SweepArgs ia = base;
+    ia.z = Z[0];
+    const int init_grid = S * std::max(1, std::min(64, (int)((3 * c->g.Nn + 255) / 256)));
+    k_init<<<init_grid, 256, 0, stream>>>(ia, P[0], P[1], Z[1], f);
+    TEM_CUDA(cudaGetLastError());
+  }
+  int nslot = S;
+  Cfg cfg = make_cfg(nslot);
+  tem::k_delta<true><<<cfg.grid, tem::NT, smem2, stream>>>(cfg.a2[0], tmZ[0]);   // delta_0
+  TEM_CUDA(cudaGetLastError());
+  long long launches = 2;
+
+  const bool trace = getenv("TEM_TRACE") != nullptr;
+  auto t_prev = std::chrono::steady_clock::now();
+  int done = 0;
+  cudaGraphExec_t graph = nullptr;
+  if (int rc = get_graph(cfg, nslot, &graph)) return rc;
+  while (done < maxit) {
+    const int chunk = std::min(kChunk, maxit - done);
+    if (chunk == kChunk) {  // kChunk is even: parity returns to 0
+      TEM_CUDA(cudaGraphLaunch(graph, stream));
+    } else {
+      for (int i = 0; i < chunk; ++i) launch_iter(cfg, (done + i) & 1, stream);
+      TEM_CUDA(cudaGetLastError());
+    }
+    launches += 2LL * chunk;
+    done += chunk;
+    TEM_CUDA(cudaMemcpyAsync(c->pinned_active, &base.ctl->n_active, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    TEM_CUDA(cudaStreamSynchronize(stream));
+    const int n_active = *c->pinned_active;
+    if (trace) {
+      const auto now = std::chrono::steady_clock::now();
+      fprintf(stderr, "[tem trace] it=%d slots=%d nzc=%d grid=%d active=%d chunk_ms=%.3f\n", done, nslot,
+              cfg.a1[0].nzc, cfg.grid, n_active,
+              std::chrono::duration<double, std::milli>(now - t_prev).count());
+      t_prev = now;
+    }
+    if (n_active == 0) break;
+    if (n_active < nslot) {
+      nslot = n_active;
+      cfg = make_cfg(nslot);
+      if (int rc = get_graph(cfg, nslot, &graph)) return rc;
+    }
+  }
+  {
+    const int fix_grid = S * std::max(1, std::min(64, (int)((3 * c->g.Nn + 255) / 256)));
+    k_xfix<<<fix_grid, 256, 0, stream>>>(base, P[1]);
+    TEM_CUDA(cudaGetLastError());
+    launches += 1;
+  }
+  TEM_CUDA(cudaEventRecord(ev1, stream));
+  return finish_solve(c, S, st, base.st, ev0, ev1, stream, launches, grid, tem::NT, iters, relres);
+}
+
+int tem_set_solver(tem_ctx* c, int solver) {
+  if (!c) return fail(TEM_EINVAL, "tem_set_solver: null context");
+  if (solver != TEM_SOLVER_SPLIT && solver != TEM_SOLVER_TWO_SWEEP)
+    return fail(TEM_EINVAL, "tem_set_solver: unknown solver " + std::to_string(solver));
+  c->solver = solver;
+  return TEM_OK;
+}
+
+int tem_get_solver(const tem_ctx* c) { return c ? c->solver : TEM_EINVAL; }
 
 int tem_last_solve_stats(const tem_ctx* c, tem_solve_stats* out) {
   if (!c || !out) return fail(TEM_EINVAL, "tem_last_solve_stats: null pointer");

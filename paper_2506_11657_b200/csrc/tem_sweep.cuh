@@ -51,18 +51,19 @@ struct ShiftState {
   double2 rho;      // r^T z
   double2 alpha;
   double2 beta;
+  double2 alpha_prev;   // alpha of the previous iteration (split solver: x every other iteration)
   double fnorm;     // ||f||_2
   double relres;    // ||r||_2 / ||f||_2
   int active;
   int iters;
   int status;       // 0 running, 1 converged, 2 breakdown
-  int pad;
+  int xlag;         // split solver: x misses alpha p of the last iteration (fixed at the end)
 };
 
 struct Control {
   double tol;
   int n_active;           // number of active shifts
-  unsigned int ticket[4];
+  unsigned int ticket[8];
   int list[32];           // the active shifts, compacted (first n_active entries)
 };
 
@@ -72,15 +73,24 @@ struct SweepArgs {
   int nslot;                   // shift slots of the grid (CTA slot a serves shift list[a])
   int ntx, nty, nzc, kchunk;   // tiles along x, y; z-chunks and their length
   const double* mass;          // [3][Nn]
-  double2* out;                // MODE 0: y; MODE 1: p_new
-  double2* x;                  // MODE 2
-  double2* z;                  // MODE 2 (in/out)
+  double2* out;                // MODE 0: y; MODE 1, 3, 4: p_new
+  double2* x;                  // MODE 2, 4
+  double2* z;                  // MODE 2 (in/out); MODE 3, 4: z_{i+1} (out)
+  const double2* zin;          // MODE 3, 4: z_i (own values; the halo comes by TMA)
+  const double2* pold;         // MODE 4: p_{i-1} (own values)
   ShiftState* st;              // [S]
   Control* ctl;
   double2* part_c;             // [gridDim]
   double* part_r;              // [gridDim]
+  double* part;                // MODE 3, 4, k_delta: [kSplitPart][pstride] per-CTA partial sums
+  int pstride;
+  int force_xdirect;           // MODE 4: always re-read p_{i-1} (tests: TEM_XDIRECT=1)
   double2 shifts[32];          // MODE 0 only
 };
+
+// Split solver (MODE 3/4 pass 1, k_delta pass 2) per-CTA partials:
+// gamma, eps, mu (re, im), ||r||^2 from pass 1; delta (re, im) from pass 2.
+constexpr int kSplitPart = 9;
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -120,6 +130,14 @@ __device__ __forceinline__ void tma_tile(void* dst, const CUtensorMap* tm, int c
 }
 
 __device__ __forceinline__ int pmod(int q, int n) { return ((q % n) + n) % n; }
+
+// 128-byte aligned view of the dynamic shared memory that stays a pointer
+// derived from the __shared__ array (so the compiler emits LDS/STS, not
+// generic LD/ST).
+__device__ __forceinline__ double2* smem_align128(unsigned char* raw) {
+  const uint32_t a = smem_u32(raw);
+  return reinterpret_cast<double2*>(raw + ((128u - (a & 127u)) & 127u));
+}
 
 __device__ __forceinline__ bool free_x(const Grid& g, int i, int j, int k) {
   return i < g.n[0] && j >= 1 && j <= g.n[1] - 1 && k >= 1 && k <= g.n[2] - 1;
@@ -186,13 +204,15 @@ struct Column {
   double cxy, cxym;         // hd_x ih_y, hd_x ih_y(j-1)
 };
 
-__device__ __forceinline__ Column make_column(const Grid& g, int tx0, int ty0) {
+// Column constants of node column (i, j); i, j may lie outside the grid
+// (halo threads of the single-pass sweep): then every weight is 0 and no
+// edge of the column is free.
+__device__ __forceinline__ Column make_column_ij(const Grid& g, int i, int j) {
   Column C;
-  const int tid = threadIdx.x;
-  C.i = tx0 + (tid % TX);
-  C.j = ty0 + (tid / TX);
-  C.c0 = ((tid / TX) + 1) * HX + (tid % TX) + 1;
-  C.in_ij = C.i < g.n[0] && C.j < g.n[1];
+  C.i = i;
+  C.j = j;
+  C.c0 = 0;
+  C.in_ij = i >= 0 && j >= 0 && i < g.n[0] && j < g.n[1];
   const double ihx = C.in_ij ? __ldg(g.ih[0] + C.i) : 0.0;
   const double ihxm = (C.in_ij && C.i >= 1) ? __ldg(g.ih[0] + C.i - 1) : 0.0;
   const double ihy = C.in_ij ? __ldg(g.ih[1] + C.j) : 0.0;
@@ -209,6 +229,13 @@ __device__ __forceinline__ Column make_column(const Grid& g, int tx0, int ty0) {
   return C;
 }
 
+__device__ __forceinline__ Column make_column(const Grid& g, int tx0, int ty0) {
+  const int tid = threadIdx.x;
+  Column C = make_column_ij(g, tx0 + (tid % TX), ty0 + (tid / TX));
+  C.c0 = ((tid / TX) + 1) * HX + (tid % TX) + 1;
+  return C;
+}
+
 // K v for the three edges of node (i, j, k) from ring tiles:
 // Xm/X0/Xp = x-comp planes k-1/k/k+1, same for Y; Zm/Z0 = z-comp layers k-1/k.
 // The 12 (edge, face) pairs touch only 9 distinct faces and 24 distinct tile
@@ -221,16 +248,17 @@ struct Edge3 {
   bool f[3];
 };
 
-__device__ __forceinline__ void stencil3(const Grid& g, const Column& C, int k, double ihz, double ihzm,
-                                         double hdz, const double2* Xm, const double2* X0,
-                                         const double2* Xp, const double2* Ym, const double2* Y0,
-                                         const double2* Yp, const double2* Zm, const double2* Z0,
-                                         Edge3& E) {
-  const int c0 = C.c0;
+// PITCH = row pitch of the tiles (in double2), c0 = index of the node in them.
+template <int PITCH>
+__device__ __forceinline__ void stencil3p(const Grid& g, const Column& C, int c0, int k, double ihz,
+                                          double ihzm, double hdz, const double2* Xm,
+                                          const double2* X0, const double2* Xp, const double2* Ym,
+                                          const double2* Y0, const double2* Yp, const double2* Zm,
+                                          const double2* Z0, Edge3& E) {
   E.f[0] = C.in_ij && free_x(g, C.i, C.j, k);
   E.f[1] = C.in_ij && free_y(g, C.i, C.j, k);
-  E.f[2] = C.in_ij && free_z(g, C.i, C.j, k);
-#define T_(P, di, dj) P[c0 + (dj) * HX + (di)]
+  E.f[2] = C.in_ij && k >= 0 && free_z(g, C.i, C.j, k);
+#define T_(P, di, dj) P[c0 + (dj) * PITCH + (di)]
   const double2 x00 = T_(X0, 0, 0), y00 = T_(Y0, 0, 0), z00 = T_(Z0, 0, 0);
   // face weights W = hdual / (mu0 A)
   const double wz = hdz * C.pxy, wz_y = hdz * C.pxym, wz_x = hdz * C.pxmy;      // Fz(m), Fz(m-ey), Fz(m-ex)
@@ -271,6 +299,113 @@ __device__ __forceinline__ void stencil3(const Grid& g, const Column& C, int k, 
   E.p[0] = x00;
   E.p[1] = y00;
   E.p[2] = z00;
+}
+
+__device__ __forceinline__ void stencil3(const Grid& g, const Column& C, int k, double ihz, double ihzm,
+                                         double hdz, const double2* Xm, const double2* X0,
+                                         const double2* Xp, const double2* Ym, const double2* Y0,
+                                         const double2* Yp, const double2* Zm, const double2* Z0,
+                                         Edge3& E) {
+  stencil3p<HX>(g, C, C.c0, k, ihz, ihzm, hdz, Xm, X0, Xp, Ym, Y0, Yp, Zm, Z0, E);
+}
+
+// v^T K v restricted to the three faces whose lower corner is this node
+// (K = T^T W T, §2.2: v^T K v = sum_f W_f C_f(v)^2 over all faces,
+// unconjugated square for the complex-symmetric form).  Summed over all
+// nodes every face is counted once; it reads only the +x, +y, +z neighbours.
+__device__ __forceinline__ double2 csq(double2 a) { return make_double2(fma(a.x, a.x, -a.y * a.y), 2.0 * a.x * a.y); }
+
+__device__ __forceinline__ double2 faces_quad(const Column& C, double ihz, double hdz, const double2* X0,
+                                              const double2* Xp, const double2* Y0, const double2* Yp,
+                                              const double2* Z0, double2 v[3]) {
+  const int c0 = C.c0;
+  const double2 x00 = X0[c0], y00 = Y0[c0], z00 = Z0[c0];
+  const double2 Fz = csub(cadd(x00, Y0[c0 + 1]), cadd(X0[c0 + HX], y00));
+  const double2 Fy = csub(cadd(z00, Xp[c0]), cadd(Z0[c0 + 1], x00));
+  const double2 Fx = csub(cadd(y00, Z0[c0 + HX]), cadd(Yp[c0], z00));
+  v[0] = x00;
+  v[1] = y00;
+  v[2] = z00;
+  double2 acc = cscale(hdz * C.pxy, csq(Fz));
+  acc = cadd(acc, cscale(C.cyx * ihz, csq(Fy)));
+  return cadd(acc, cscale(C.cxy * ihz, csq(Fx)));
+}
+
+// ---------------------------------------------------------------- pass 2
+// k_delta: delta = z^T A z of the split solver, per shift, from the node's own
+// faces (faces_quad) and the mass term.  It reads z once (16 B per unknown per
+// shift) with a +1 halo; plane sets q = {X(q), Y(q), Z(q)} in a 4-deep ring
+// (step k reads sets k and k+1, sets k+2 and k+3 in flight): 12 tiles, 66 KB,
+// three CTAs per SM.
+constexpr int R_D = 4;
+constexpr size_t kSmemDelta = 128 + (size_t)3 * R_D * TILE_STRIDE;
+
+// Split solver finalisation (last CTA of pass 2): per-shift sums of the pass-1
+// partials (gamma, eps, mu, ||r||^2) and the pass-2 partial delta, then
+//   beta = gamma / gamma_prev,  p^T A p = delta + beta (2 eps + beta mu),
+//   alpha = gamma / p^T A p     (reading R10)
+// PRIME (after k_init): alpha_0 = gamma_0 / delta_0.
+template <bool PRIME>
+__device__ void finalize_split(const SweepArgs& A) {
+  const int S = A.S, ns = A.nslot;
+  const int n_list = A.ctl->n_active;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nblk = gridDim.x;
+  for (int a = warp; a < ns && a < n_list; a += NT / 32) {
+    ShiftState& sq = A.st[A.ctl->list[a]];
+    if (!sq.active) continue;
+    double v[kSplitPart];
+#pragma unroll
+    for (int t = 0; t < kSplitPart; ++t) {
+      double acc = 0.0;
+      if (!PRIME || t >= 7)
+        for (int b = a + lane * ns; b < nblk; b += 32 * ns) acc += __ldcg(A.part + t * A.pstride + b);
+      v[t] = warp_sum(acc);
+    }
+    if (lane != 0) continue;
+    const double2 gam = make_double2(v[0], v[1]), eps = make_double2(v[2], v[3]);
+    const double2 mu = make_double2(v[4], v[5]), del = make_double2(v[7], v[8]);
+    if (PRIME) {
+      if (del.x == 0.0 && del.y == 0.0) {
+        sq.active = 0;
+        sq.status = 2;
+      } else {
+        sq.alpha = cdiv(sq.rho, del);
+        sq.alpha_prev = czero();
+        sq.beta = czero();
+      }
+      continue;
+    }
+    sq.iters += 1;
+    sq.relres = sqrt(v[6]) / sq.fnorm;
+    if (sq.relres <= A.ctl->tol) {
+      sq.active = 0;
+      sq.status = 1;
+    } else if ((gam.x == 0.0 && gam.y == 0.0) || (sq.rho.x == 0.0 && sq.rho.y == 0.0)) {
+      sq.active = 0;
+      sq.status = 2;
+    } else {
+      const double2 beta = cdiv(gam, sq.rho);
+      const double2 den = cadd(del, cmul(beta, cadd(cscale(2.0, eps), cmul(beta, mu))));
+      if (den.x == 0.0 && den.y == 0.0) {
+        sq.active = 0;
+        sq.status = 2;
+      } else {
+        sq.beta = beta;
+        sq.alpha_prev = sq.alpha;
+        sq.alpha = cdiv(gam, den);
+        sq.rho = gam;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int na = 0;
+    for (int q = 0; q < S; ++q)
+      if (A.st[q].active) A.ctl->list[na++] = q;
+    A.ctl->n_active = na;
+    A.ctl->ticket[PRIME ? 6 : 5] = 0;
+  }
 }
 
 // Finalisation by the last CTA: per-shift sums of the per-CTA partials (the
@@ -357,9 +492,10 @@ template <int MODE>
 __global__ void __launch_bounds__(NT, kMinBlocks) k_sweep(const __grid_constant__ SweepArgs A,
                                                  const __grid_constant__ CUtensorMap tmv,
                                                  const __grid_constant__ CUtensorMap tmz) {
-  constexpr bool kZ = (MODE == 1);
+  constexpr bool kZ = (MODE == 1 || MODE == 3 || MODE == 4);   // p_new = z + beta p_old formed in smem
+  constexpr bool kUpd = (MODE == 3 || MODE == 4);               // split pass 1: full update
   extern __shared__ unsigned char smem_raw[];
-  double2* ring = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  double2* ring = smem_align128(smem_raw);
   double2* rX = ring;                        // [R_XY] slots
   double2* rY = ring + R_XY * TS2;           // [R_XY]
   double2* rZ = ring + 2 * R_XY * TS2;       // [R_Z]
@@ -374,7 +510,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) k_sweep(const __grid_constant_
   block_coords(A, a, tx0, ty0, kb, ke);
   const int tid = threadIdx.x;
 
-  double2 sh = czero(), alpha = czero(), beta = czero();
+  double2 sh = czero(), alpha = czero(), beta = czero(), alpha_prev = czero();
   bool live;
   int s = a;
   if (MODE == 0) {
@@ -388,11 +524,22 @@ __global__ void __launch_bounds__(NT, kMinBlocks) k_sweep(const __grid_constant_
       sh = st.s;
       alpha = st.alpha;
       beta = st.beta;
+      alpha_prev = st.alpha_prev;
       live = st.active != 0;
     }
   }
-  double2 acc_c = czero();
+  double2 acc_c = czero(), acc_e = czero(), acc_m = czero();
   double acc_r = 0.0;
+  // MODE 4: x_{i+1} = x_{i-1} + (alpha_i + a/beta_i) p_i - (a/beta_i) z_i, a = alpha_{i-1}
+  // (exact rewrite of alpha_{i-1} p_{i-1} + alpha_i p_i); when |beta_i| < 1/8 the
+  // subtraction p_i - z_i loses digits and p_{i-1} is re-read instead (x_direct).
+  const bool x_direct = MODE == 4 && (A.force_xdirect || beta.x * beta.x + beta.y * beta.y < 1.0 / 64.0);
+  double2 xc_p = czero(), xc_z = czero();
+  if (MODE == 4 && !x_direct) {
+    xc_z = cdiv(alpha_prev, beta);
+    xc_p = cadd(alpha, xc_z);
+    xc_z = make_double2(-xc_z.x, -xc_z.y);
+  }
 
   if (live) {
     const Column C = make_column(g, tx0, ty0);
@@ -482,6 +629,8 @@ __global__ void __launch_bounds__(NT, kMinBlocks) k_sweep(const __grid_constant_
           xN[c] = ok ? A.x[vs + slot] : czero();
           zN[c] = ok ? A.z[vs + slot] : czero();
         }
+        if (kUpd) zN[c] = ok ? __ldcg(A.zin + vs + slot) : czero();
+        if (MODE == 4) xN[c] = ok ? A.x[vs + slot] : czero();
       }
     };
     load_centre(kb);
@@ -500,7 +649,23 @@ __global__ void __launch_bounds__(NT, kMinBlocks) k_sweep(const __grid_constant_
         if (!E.f[c]) continue;
         const long long e = vs + (long long)c * g.Nn + node;
         const double2 q = cfma(sh, cscale(mN[c], E.p[c]), E.q[c]);   // (K + s M) v
-        if (MODE == 0) {
+        if (kUpd) {
+          const double2 D = make_double2(E.kd[c] + mN[c] * sh.x, mN[c] * sh.y);
+          const double2 zn = csub(zN[c], cmul(alpha, cmul(q, crcp(D))));   // z_i - alpha D^-1 A p_i
+          A.out[e] = E.p[c];                                              // p_i
+          A.z[e] = zn;                                                    // z_{i+1}
+          if (MODE == 4) {   // x_{i+1} = x_{i-1} + alpha_{i-1} p_{i-1} + alpha_i p_i
+            if (x_direct)
+              A.x[e] = cfma(alpha, E.p[c], cfma(alpha_prev, __ldcg(A.pold + e), xN[c]));
+            else   // p_{i-1} = (p_i - z_i) / beta_i: no re-read of p_{i-1}
+              A.x[e] = cfma(xc_z, zN[c], cfma(xc_p, E.p[c], xN[c]));
+          }
+          const double2 rn = cmul(D, zn);                                 // r_{i+1} = D z_{i+1}
+          acc_c = cfma(rn, zn, acc_c);                                    // gamma_{i+1}
+          acc_r += rn.x * rn.x + rn.y * rn.y;
+          acc_e = cfma(zn, q, acc_e);                                     // z_{i+1}^T A p_i
+          acc_m = cfma(E.p[c], q, acc_m);                                 // p_i^T A p_i
+        } else if (MODE == 0) {
           A.out[e] = q;
         } else if (MODE == 1) {
           A.out[e] = E.p[c];                 // p_new
@@ -527,6 +692,24 @@ __global__ void __launch_bounds__(NT, kMinBlocks) k_sweep(const __grid_constant_
     }
   }
   if (MODE == 0) return;
+  if (kUpd) {
+    __shared__ double red9[kSplitPart * NT / 32];
+    double v[kSplitPart] = {acc_c.x, acc_c.y, acc_e.x, acc_e.y, acc_m.x, acc_m.y, acc_r, 0.0, 0.0};
+    constexpr int t0 = 0, t1 = 7;
+    for (int t = t0; t < t1; ++t)
+      for (int o = 16; o > 0; o >>= 1) v[t] += __shfl_down_sync(0xffffffffu, v[t], o);
+    const int w = tid >> 5, l = tid & 31;
+    __syncthreads();
+    if (l == 0)
+      for (int t = t0; t < t1; ++t) red9[kSplitPart * w + t] = v[t];
+    __syncthreads();
+    if (tid < t1 - t0) {
+      double acc = 0.0;
+      for (int q = 0; q < NT / 32; ++q) acc += red9[kSplitPart * q + t0 + tid];
+      A.part[(t0 + tid) * A.pstride + blockIdx.x] = acc;
+    }
+    return;
+  }
   block_sum_n<NT>(acc_c, acc_r, red);
   if (tid == 0) {
     A.part_c[blockIdx.x] = acc_c;
@@ -534,6 +717,97 @@ __global__ void __launch_bounds__(NT, kMinBlocks) k_sweep(const __grid_constant_
   }
   if (!last_block(&A.ctl->ticket[MODE])) return;
   finalize<MODE>(A);
+}
+
+}  // namespace tem
+
+namespace tem {
+
+template <bool PRIME>
+__global__ void __launch_bounds__(NT, 3) k_delta(const __grid_constant__ SweepArgs A,
+                                                 const __grid_constant__ CUtensorMap tmv) {
+  extern __shared__ unsigned char smem_raw[];
+  double2* ring = smem_align128(smem_raw);   // [R_D][3] tiles
+  __shared__ __align__(8) uint64_t bar[R_D];
+  __shared__ double red[3 * NT / 32];
+  __shared__ double zih[kMaxChunk];         // ih_z[k]   for k = kb .. ke-1
+  __shared__ double zhd[kMaxChunk];         // hdm_z[k]  for k = kb .. ke-1
+
+  const Grid& g = A.g;
+  int a, tx0, ty0, kb, ke;
+  block_coords(A, a, tx0, ty0, kb, ke);
+  const int tid = threadIdx.x;
+  bool live = a < A.ctl->n_active;
+  int s = 0;
+  double2 sh = czero();
+  if (live) {
+    s = A.ctl->list[a];
+    sh = A.st[s].s;
+    live = A.st[s].active != 0;
+  }
+  double2 acc = czero();
+  if (live) {
+    const Column C = make_column(g, tx0, ty0);
+    for (int q = tid; q < ke - kb; q += NT) {
+      zih[q] = __ldg(g.ih[2] + kb + q);
+      zhd[q] = __ldg(g.hdm[2] + kb + q);
+    }
+    auto issue = [&](int q) {
+      const int b = q % R_D;
+      mbar_expect_tx(&bar[b], 3 * TILE_BYTES);
+      const int cx = 2 * (tx0 - 1), cy = ty0 - 1;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) tma_tile(ring + (b * 3 + c) * TS2, &tmv, cx, cy, q, c, s, &bar[b]);
+    };
+    uint32_t phase = 0;
+    auto wait_set = [&](int q) {
+      const int b = q % R_D;
+      mbar_wait(&bar[b], (phase >> b) & 1u);
+      phase ^= 1u << b;
+    };
+    if (tid == 0) {
+      for (int q = 0; q < R_D; ++q) mbar_init(&bar[q], 1);
+      fence_barrier_init();
+    }
+    __syncthreads();
+    if (tid == 0)
+      for (int q = kb; q <= min(kb + 3, ke); ++q) issue(q);
+    wait_set(kb);
+    const long long plane = (long long)(g.n[0] + 1) * (g.n[1] + 1);
+    const double* mcol = A.mass + (C.in_ij ? (long long)C.j * (g.n[0] + 1) + C.i : 0);
+    double mN[3];
+    auto load_mass = [&](int k) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) mN[c] = C.in_ij ? __ldg(mcol + k * plane + c * g.Nn) : 0.0;
+    };
+    load_mass(kb);
+#pragma unroll 1
+    for (int k = kb; k < ke; ++k) {
+      wait_set(k + 1);
+      const double2* S0 = ring + (k % R_D) * 3 * TS2;
+      const double2* S1 = ring + ((k + 1) % R_D) * 3 * TS2;
+      double2 v[3];
+      const double2 fq = faces_quad(C, zih[k - kb], zhd[k - kb], S0, S1, S0 + TS2, S1 + TS2, S0 + 2 * TS2, v);
+      double2 mq = cscale(mN[0], csq(v[0]));
+      mq = cfma(make_double2(mN[1], 0.0), csq(v[1]), mq);
+      mq = cfma(make_double2(mN[2], 0.0), csq(v[2]), mq);
+      acc = cadd(acc, cfma(sh, mq, fq));
+      if (k + 1 < ke) load_mass(k + 1);
+      __syncthreads();   // set k no longer read
+      if (tid == 0 && k + 4 <= ke) {
+        fence_proxy_async();
+        issue(k + 4);
+      }
+    }
+  }
+  double rdum = 0.0;
+  block_sum_n<NT>(acc, rdum, red);
+  if (tid == 0) {
+    A.part[7 * A.pstride + blockIdx.x] = acc.x;
+    A.part[8 * A.pstride + blockIdx.x] = acc.y;
+  }
+  if (!last_block(&A.ctl->ticket[PRIME ? 6 : 5])) return;
+  finalize_split<PRIME>(A);
 }
 
 }  // namespace tem

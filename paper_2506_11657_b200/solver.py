@@ -125,6 +125,20 @@ class TemForward:
         self.n_unknowns = int(self.lib.tem_num_unknowns(h))
         self._work = {}
 
+    SOLVERS = {"split": 0, "two_sweep": 1}   # TEM_SOLVER_* of include/tem_b200.h
+
+    @property
+    def solver(self) -> str:
+        """COCG iteration scheme of tem_cocg_solve (tem_set_solver)."""
+        code = int(self.lib.tem_get_solver(self._h))
+        return {v: k for k, v in self.SOLVERS.items()}[code]
+
+    @solver.setter
+    def solver(self, name: str):
+        if name not in self.SOLVERS:
+            raise ValueError(f"solver must be one of {sorted(self.SOLVERS)}")
+        _lib.check(self.lib.tem_set_solver(self._h, self.SOLVERS[name]))
+
     def close(self):
         if self._h:
             self.lib.tem_destroy(self._h)

@@ -66,6 +66,13 @@ def test_invalid_arguments_rejected_before_launch(lib):
     assert lib.tem_cocg_workspace_bytes(None, 4) == 0
 
 
+def test_solver_selection_argument_checks(lib):
+    # NULL context: rejected before any CUDA call
+    assert lib.tem_set_solver(None, 0) == -1
+    assert lib.tem_get_solver(None) == -1
+    assert b"tem_set_solver" in lib.tem_last_error()
+
+
 def test_binding_refuses_cpu_tensors():
     import torch
     from paper_2506_11657_b200.solver import _need_cuda

@@ -25,11 +25,12 @@ from paper_2506_11657_b200 import RationalTable, TemForward  # noqa: E402
 _CACHE = {}
 
 
-def _solved(name):
-    if name not in _CACHE:
+def _solved(name, solver="split"):
+    if (name, solver) not in _CACHE:
         wl = make_workload(name)
         table = RationalTable.load(name)
         fw = TemForward(wl.grid.hx, wl.grid.hy, wl.grid.hz)
+        fw.solver = solver
         sigma = torch.from_numpy(fw.sigma_layout(wl.sigma)).cuda()
         f = torch.from_numpy(fw.source_vector(wl.source)).cuda()
         mass = fw.edge_mass(sigma)
@@ -37,13 +38,14 @@ def _solved(name):
         asm = yee.assemble(wl)
         slots = fw.slot(*asm.keys())
         _CACHE.clear()
-        _CACHE[name] = (wl, table, fw, mass, x, iters, relres, asm, slots)
-    return _CACHE[name]
+        _CACHE[(name, solver)] = (wl, table, fw, mass, x, iters, relres, asm, slots)
+    return _CACHE[(name, solver)]
 
 
-@pytest.mark.parametrize("name", ["layered", "hetero", "large"])
-def test_true_residual_every_shift(name):
-    wl, table, fw, mass, x, iters, relres, asm, slots = _solved(name)
+@pytest.mark.parametrize("name,solver", [("layered", "split"), ("hetero", "split"), ("large", "split"),
+                                         ("layered", "two_sweep")])
+def test_true_residual_every_shift(name, solver):
+    wl, table, fw, mass, x, iters, relres, asm, slots = _solved(name, solver)
     assert np.all(relres <= 1e-10) and np.all(iters > 0)
     for i, s in enumerate(table.shifts):
         xi = x[i].cpu().numpy()[slots]

@@ -30,8 +30,12 @@ from paper_2506_11657_b200 import RationalTable, TemForward  # noqa: E402
 from paper_2506_11657_b200 import _lib  # noqa: E402
 
 
-def _setup(wl, table_name=None, table=None):
+SOLVERS = ["split", "two_sweep"]   # TEM_SOLVER_* (include/tem_b200.h)
+
+
+def _setup(wl, table_name=None, table=None, solver="split"):
     fw = TemForward(wl.grid.hx, wl.grid.hy, wl.grid.hz)
+    fw.solver = solver
     asm = yee.assemble(wl)
     slots = fw.slot(*asm.keys())
     if table is None:
@@ -106,8 +110,9 @@ def _air_edges(asm, wl):
     return ((c == 2) & (k >= ks)) | ((c != 2) & (k > ks))
 
 
+@pytest.mark.parametrize("solver", SOLVERS)
 @pytest.mark.parametrize("name", ["tiny", "ragged", "ragged2"])
-def test_forward_parity_vs_exact_lu(name):
+def test_forward_parity_vs_exact_lu(name, solver):
     """Tight solve (tol 1e-14) vs the oracle's exact LU, channel fields u(t_j):
     relative L2 <= 1e-7 at EVERY channel over the conducting (non-air)
     edges, and <= 1e-7 of the summand scale T_j over all edges.  The air's
@@ -115,7 +120,7 @@ def test_forward_parity_vs_exact_lu(name):
     solver (reading R6); their plain relative error is reported, not gated."""
     wl = WORKLOADS[name]()
     table = RationalTable.load("tiny") if name == "tiny" else _oracle_table(wl)
-    fw, asm, slots, table, sigma, f = _setup(wl, table=table)
+    fw, asm, slots, table, sigma, f = _setup(wl, table=table, solver=solver)
     mass = fw.edge_mass(sigma)
     x, iters, relres = fw.cocg(mass, f, table.shifts, tol=1e-14, maxit=50000,
                                raise_on_noconv=False)
@@ -138,13 +143,14 @@ def test_forward_parity_vs_exact_lu(name):
           f"term max {rel_term.max():.2e}, plain (incl. air) max {plain.max():.2e}")
 
 
+@pytest.mark.parametrize("solver", SOLVERS)
 @pytest.mark.parametrize("name", ["tiny", "ragged", "block"])
-def test_cocg_default_tolerance(name):
+def test_cocg_default_tolerance(name, solver):
     """North-star tolerance 1e-10: every shift converged, true residual
     (oracle CSR) within the tolerance, M-norm agreement with the oracle."""
     wl = make_workload(name) if name in ("tiny", "block") else WORKLOADS[name]()
     table = RationalTable.load(name) if name in ("tiny", "block") else _oracle_table(wl)
-    fw, asm, slots, table, sigma, f = _setup(wl, table=table)
+    fw, asm, slots, table, sigma, f = _setup(wl, table=table, solver=solver)
     mass = fw.edge_mass(sigma)
     x, iters, relres = fw.cocg(mass, f, table.shifts, tol=1e-10, maxit=50000)
     assert np.all(relres <= 1e-10) and np.all(iters > 0)
@@ -175,9 +181,10 @@ def test_synthesis_exact():
     assert np.all(u[:, mask] == 0)
 
 
-def test_edge_cases():
+@pytest.mark.parametrize("solver", SOLVERS)
+def test_edge_cases(solver):
     wl = make_workload("tiny")
-    fw, asm, slots, table, sigma, f = _setup(wl)
+    fw, asm, slots, table, sigma, f = _setup(wl, solver=solver)
     mass = fw.edge_mass(sigma)
     # zero source: converged at iteration 0 with x = 0
     x, iters, relres = fw.cocg(mass, torch.zeros_like(f), table.shifts)
@@ -205,9 +212,10 @@ def test_forward_host_matches_device_path():
     np.testing.assert_array_equal(u_dev.cpu().numpy(), u_host)
 
 
-def test_deterministic_repeat():
+@pytest.mark.parametrize("solver", SOLVERS)
+def test_deterministic_repeat(solver):
     wl = make_workload("block")
-    fw, asm, slots, table, sigma, f = _setup(wl)
+    fw, asm, slots, table, sigma, f = _setup(wl, solver=solver)
     mass = fw.edge_mass(sigma)
     x1, i1, _ = fw.cocg(mass, f, table.shifts)
     x2, i2, _ = fw.cocg(mass, f, table.shifts)
@@ -215,7 +223,8 @@ def test_deterministic_repeat():
     assert torch.equal(x1, x2)
 
 
-def test_tall_grid_forced_chunks_vs_oracle_cocg():
+@pytest.mark.parametrize("solver", SOLVERS)
+def test_tall_grid_forced_chunks_vs_oracle_cocg(solver):
     """nz = 136 > kMaxChunk (128) forces z-chunking in every launch; 32 shifts
     (the ABI maximum) on a ragged 19x15x136 grid with random conductivity,
     full COCG to 1e-12 vs the oracle's own COCG to 1e-13 for two shifts:
@@ -226,7 +235,7 @@ def test_tall_grid_forced_chunks_vs_oracle_cocg():
     S = 32
     shifts = (10 ** rng.uniform(2.5, 5.5, S)) * np.exp(1j * rng.uniform(-1.2, 1.2, S))
     table = RationalTable(shifts, np.ones((S, 1)), np.zeros(S, bool), [1.0])
-    fw, asm, slots, table, sigma, f = _setup(wl, table=table)
+    fw, asm, slots, table, sigma, f = _setup(wl, table=table, solver=solver)
     mass = fw.edge_mass(sigma)
     x, iters, relres = fw.cocg(mass, f, table.shifts, tol=1e-12, maxit=100000)
     xg = x.cpu().numpy()[:, slots].T
@@ -238,3 +247,50 @@ def test_tall_grid_forced_chunks_vs_oracle_cocg():
         relM = ofw.m_norm(asm, xg[:, i] - xo) / ofw.m_norm(asm, xo)
         rel_e = np.linalg.norm((xg[:, i] - xo)[earth]) / np.linalg.norm(xo[earth])
         assert relM < 1e-9 and rel_e < 1e-8, (i, relM, rel_e)
+
+
+@pytest.mark.parametrize("maxit", [5, 6, 37, 38])
+def test_split_iterate_bookkeeping(maxit, monkeypatch):
+    """The split scheme advances x every second iteration (and re-forms
+    p_{i-1} from p_i, z_i); stopped after an odd or even number of
+    iterations, x must be the COCG iterate whose residual the recursion
+    reports: ||f - A x|| / ||f|| (oracle CSR) equals relres, and both the
+    p-re-reading and the re-forming path give the same x."""
+    wl = make_workload("block")
+    fw, asm, slots, table, sigma, f = _setup(wl, solver="split")
+    mass = fw.edge_mass(sigma)
+    x, iters, relres = fw.cocg(mass, f, table.shifts, tol=1e-14, maxit=maxit,
+                               raise_on_noconv=False)
+    assert np.all(iters == maxit)
+    xg = x.cpu().numpy()[:, slots].T
+    for i, s in enumerate(table.shifts):
+        true = ofw.relative_residual(asm, s, xg[:, i])
+        assert abs(true - relres[i]) <= 1e-6 * relres[i], (i, true, relres[i])
+    monkeypatch.setenv("TEM_XDIRECT", "1")
+    x2, iters2, relres2 = fw.cocg(mass, f, table.shifts, tol=1e-14, maxit=maxit,
+                                  raise_on_noconv=False)
+    d = ((x2 - x).abs().pow(2).sum(1).sqrt() / x.abs().pow(2).sum(1).sqrt()).cpu().numpy()
+    assert np.all(d <= 1e-12), d
+
+
+def test_split_and_two_sweep_agree():
+    """Both COCG schemes converge to the same solutions (M-norm, conducting
+    edges) on the block model at the north-star tolerance."""
+    wl = make_workload("block")
+    out = {}
+    for solver in SOLVERS:
+        fw, asm, slots, table, sigma, f = _setup(wl, solver=solver)
+        mass = fw.edge_mass(sigma)
+        x, iters, relres = fw.cocg(mass, f, table.shifts, tol=1e-12, maxit=50000)
+        out[solver] = x.cpu().numpy()[:, slots].T
+    # both stop at recursive residual 1e-12; their errors (and so their
+    # difference) are that times the conditioning of the shifted system, the
+    # same bar test_cocg_default_tolerance applies against the exact LU
+    earth = ~_air_edges(asm, wl)
+    relM, rele = [], []
+    for i in range(table.n_shift):
+        a, b = out["split"][:, i], out["two_sweep"][:, i]
+        relM.append(ofw.m_norm(asm, a - b) / ofw.m_norm(asm, b))
+        rele.append(np.linalg.norm((a - b)[earth]) / np.linalg.norm(b[earth]))
+    print(f"split vs two_sweep: M-norm max {max(relM):.2e}, conducting edges max {max(rele):.2e}")
+    assert max(relM) <= 1e-6 and max(rele) <= 1e-9, (relM, rele)   # measured 1.5e-8, 4.4e-11
