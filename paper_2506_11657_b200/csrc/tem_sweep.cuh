@@ -129,7 +129,8 @@ __device__ __forceinline__ void tma_tile(void* dst, const CUtensorMap* tm, int c
       : "memory");
 }
 
-__device__ __forceinline__ int pmod(int q, int n) { return ((q % n) + n) % n; }
+// q mod n for q >= -8n (ring slots of plane sets; sets start at kb - 2 >= -2)
+__device__ __forceinline__ int pmod(int q, int n) { return (int)((unsigned)(q + 8 * n) % (unsigned)n); }
 
 // 128-byte aligned view of the dynamic shared memory that stays a pointer
 // derived from the __shared__ array (so the compiler emits LDS/STS, not
@@ -635,19 +636,29 @@ __global__ void __launch_bounds__(NT, kMinBlocks) k_sweep(const __grid_constant_
     };
     load_centre(kb);
 
+    // ring slots of the planes the stencil reads: X, Y of k-1, k, k+1 (sets
+    // k-2, k-1, k), Z of k-1, k (sets k-1, k); rotated once per step
+    int sxm = pmod(kb - 2, R_XY), sx0 = pmod(kb - 1, R_XY), sxp = pmod(kb, R_XY);
+    int szm = pmod(kb - 1, R_Z), sz0 = pmod(kb, R_Z);
+    const long long col = vs + (long long)C.j * nx1 + C.i;   // own column, component 0, plane 0
+    const long long plane = (long long)nx1 * ny1;
+#pragma unroll 1
     for (int k = kb; k < ke; ++k) {
       if (!kZ) wait_set(k);
       Edge3 E;
-      stencil3(g, C, k, zih[k - kb + 1], zih[k - kb], zhd[k - kb],
-               rX + pmod(k - 2, R_XY) * TS2, rX + pmod(k - 1, R_XY) * TS2,
-               rX + pmod(k, R_XY) * TS2, rY + pmod(k - 2, R_XY) * TS2,
-               rY + pmod(k - 1, R_XY) * TS2, rY + pmod(k, R_XY) * TS2,
-               rZ + pmod(k - 1, R_Z) * TS2, rZ + pmod(k, R_Z) * TS2, E);
-      const long long node = node_of(k);
+      stencil3(g, C, k, zih[k - kb + 1], zih[k - kb], zhd[k - kb], rX + sxm * TS2, rX + sx0 * TS2,
+               rX + sxp * TS2, rY + sxm * TS2, rY + sx0 * TS2, rY + sxp * TS2, rZ + szm * TS2,
+               rZ + sz0 * TS2, E);
+      sxm = sx0;
+      sx0 = sxp;
+      sxp = sxp + 1 == R_XY ? 0 : sxp + 1;
+      szm = sz0;
+      sz0 = sz0 + 1 == R_Z ? 0 : sz0 + 1;
+      const long long ek = col + (long long)k * plane;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         if (!E.f[c]) continue;
-        const long long e = vs + (long long)c * g.Nn + node;
+        const long long e = ek + (long long)c * g.Nn;
         const double2 q = cfma(sh, cscale(mN[c], E.p[c]), E.q[c]);   // (K + s M) v
         if (kUpd) {
           const double2 D = make_double2(E.kd[c] + mN[c] * sh.x, mN[c] * sh.y);
