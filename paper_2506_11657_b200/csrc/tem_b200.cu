@@ -258,6 +258,7 @@ struct tem_ctx {
   tem_solve_stats stats{};
   int sweep_per_sm = 2;             // resident sweep CTAs per SM (occupancy of k_sweep<1>)
   int solver = TEM_SOLVER_SPLIT;
+  int band = 4;                     // tile rows per band of the sweep block order (block_coords)
 };
 
 static int check_S(int S) {
@@ -275,6 +276,7 @@ static void sweep_geometry(const tem_ctx* c, int S, int nslot, tem::SweepArgs& A
   A.g = c->g;
   A.S = S;
   A.nslot = nslot;
+  A.band = c->band;
   A.ntx = (c->g.n[0] + tem::TX - 1) / tem::TX;
   A.nty = (c->g.n[1] + tem::TY - 1) / tem::TY;
   const int target = 4 * c->num_sms * c->sweep_per_sm;
@@ -406,6 +408,7 @@ int tem_create(int nx, int ny, int nz, const double* hx, const double* hy, const
     tem_destroy(c);
     return rc;
   }
+  if (const char* env = getenv("TEM_BAND")) c->band = atoi(env);   // experiments
   {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tem::k_sweep<1>, tem::NT, tem::kSmemDirap);

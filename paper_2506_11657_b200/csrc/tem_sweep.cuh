@@ -84,6 +84,7 @@ struct SweepArgs {
   double* part_r;              // [gridDim]
   double* part;                // MODE 3, 4, k_delta: [kSplitPart][pstride] per-CTA partial sums
   int pstride;
+  int band;                    // tile rows per band of the block order (block_coords)
   int force_xdirect;           // MODE 4: always re-read p_{i-1} (tests: TEM_XDIRECT=1)
   double2 shifts[32];          // MODE 0 only
 };
@@ -351,7 +352,7 @@ __device__ void finalize_split(const SweepArgs& A) {
   const int S = A.S, ns = A.nslot;
   const int n_list = A.ctl->n_active;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nblk = gridDim.x;
+  const int per = gridDim.x / ns;   // blocks per shift slot (pidx of block_coords)
   for (int a = warp; a < ns && a < n_list; a += NT / 32) {
     ShiftState& sq = A.st[A.ctl->list[a]];
     if (!sq.active) continue;
@@ -360,7 +361,7 @@ __device__ void finalize_split(const SweepArgs& A) {
     for (int t = 0; t < kSplitPart; ++t) {
       double acc = 0.0;
       if (!PRIME || t >= 7)
-        for (int b = a + lane * ns; b < nblk; b += 32 * ns) acc += __ldcg(A.part + t * A.pstride + b);
+        for (int b = a * per + lane; b < (a + 1) * per; b += 32) acc += __ldcg(A.part + t * A.pstride + b);
       v[t] = warp_sum(acc);
     }
     if (lane != 0) continue;
@@ -417,12 +418,12 @@ __device__ void finalize(const SweepArgs& A) {
   const int S = A.S, ns = A.nslot;
   const int n_list = A.ctl->n_active;   // as read by every CTA of this launch
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nblk = gridDim.x;
+  const int per = gridDim.x / ns;   // blocks per shift slot (pidx of block_coords)
   for (int a = warp; a < ns && a < n_list; a += NT / 32) {
     ShiftState& sq = A.st[A.ctl->list[a]];
     if (!sq.active) continue;
     double cx = 0, cy = 0, cr = 0;
-    for (int b = a + lane * ns; b < nblk; b += 32 * ns) {
+    for (int b = a * per + lane; b < (a + 1) * per; b += 32) {
       const double2 v = __ldcg(A.part_c + b);
       cx += v.x;
       cy += v.y;
@@ -467,18 +468,40 @@ __device__ void finalize(const SweepArgs& A) {
   }
 }
 
+// block -> (z-chunk, band of `band` tile rows, shift slot, tile row, tile
+// column), column fastest.  The CTAs of one band run together for all shift
+// slots, so (i) the S CTAs of a tile share its coefficients (mass) through L2
+// and (ii) a tile's +-y halo rows were streamed moments earlier by its
+// neighbour in the band (L2 hits instead of DRAM re-reads).  band = 0: the
+// slot-fastest order (slot, then column, then row).  pidx: index of the
+// block's reduction partials, slot-major ([slot][tile and chunk]).
 __device__ __forceinline__ void block_coords(const SweepArgs& A, int& a, int& tx0, int& ty0, int& kb,
-                                             int& ke) {
-  // block -> (z-chunk, xy tile, shift slot), slot fastest so that the CTAs of
-  // one tile for all shifts run together and share its coefficients via L2
-  const int ns = A.nslot;
-  a = blockIdx.x % ns;
-  const int xy = (blockIdx.x / ns) % (A.ntx * A.nty);
-  const int zc = blockIdx.x / (ns * A.ntx * A.nty);
-  tx0 = (xy % A.ntx) * TX;
-  ty0 = (xy / A.ntx) * TY;
+                                             int& ke, int& pidx) {
+  const int ns = A.nslot, ntx = A.ntx, nty = A.nty;
+  const int per_z = ns * ntx * nty;
+  const int zc = blockIdx.x / per_z;
+  int r = blockIdx.x - zc * per_z;
+  int tx, ty;
+  if (A.band <= 0) {
+    a = r % ns;
+    const int xy = r / ns;
+    tx = xy % ntx;
+    ty = xy / ntx;
+  } else {
+    const int per_band = A.band * ntx * ns;
+    const int band = r / per_band;
+    r -= band * per_band;
+    const int rows = min(A.band, nty - band * A.band);
+    a = r / (rows * ntx);
+    const int t = r - a * rows * ntx;
+    ty = band * A.band + t / ntx;
+    tx = t % ntx;
+  }
+  tx0 = tx * TX;
+  ty0 = ty * TY;
   kb = zc * A.kchunk;
   ke = min(kb + A.kchunk, A.g.n[2]);
+  pidx = a * (A.nzc * ntx * nty) + (zc * nty + ty) * ntx + tx;
 }
 
 // ---------------------------------------------------------------- sweeps
@@ -508,7 +531,8 @@ __global__ void __launch_bounds__(NT, kMinBlocks) k_sweep(const __grid_constant_
 
   const Grid& g = A.g;
   int a, tx0, ty0, kb, ke;
-  block_coords(A, a, tx0, ty0, kb, ke);
+  int pidx;
+  block_coords(A, a, tx0, ty0, kb, ke, pidx);
   const int tid = threadIdx.x;
 
   double2 sh = czero(), alpha = czero(), beta = czero(), alpha_prev = czero();
@@ -717,14 +741,14 @@ __global__ void __launch_bounds__(NT, kMinBlocks) k_sweep(const __grid_constant_
     if (tid < t1 - t0) {
       double acc = 0.0;
       for (int q = 0; q < NT / 32; ++q) acc += red9[kSplitPart * q + t0 + tid];
-      A.part[(t0 + tid) * A.pstride + blockIdx.x] = acc;
+      A.part[(t0 + tid) * A.pstride + pidx] = acc;
     }
     return;
   }
   block_sum_n<NT>(acc_c, acc_r, red);
   if (tid == 0) {
-    A.part_c[blockIdx.x] = acc_c;
-    A.part_r[blockIdx.x] = acc_r;
+    A.part_c[pidx] = acc_c;
+    A.part_r[pidx] = acc_r;
   }
   if (!last_block(&A.ctl->ticket[MODE])) return;
   finalize<MODE>(A);
@@ -746,7 +770,8 @@ __global__ void __launch_bounds__(NT, 3) k_delta(const __grid_constant__ SweepAr
 
   const Grid& g = A.g;
   int a, tx0, ty0, kb, ke;
-  block_coords(A, a, tx0, ty0, kb, ke);
+  int pidx;
+  block_coords(A, a, tx0, ty0, kb, ke, pidx);
   const int tid = threadIdx.x;
   bool live = a < A.ctl->n_active;
   int s = 0;
@@ -814,8 +839,8 @@ __global__ void __launch_bounds__(NT, 3) k_delta(const __grid_constant__ SweepAr
   double rdum = 0.0;
   block_sum_n<NT>(acc, rdum, red);
   if (tid == 0) {
-    A.part[7 * A.pstride + blockIdx.x] = acc.x;
-    A.part[8 * A.pstride + blockIdx.x] = acc.y;
+    A.part[7 * A.pstride + pidx] = acc.x;
+    A.part[8 * A.pstride + pidx] = acc.y;
   }
   if (!last_block(&A.ctl->ticket[PRIME ? 6 : 5])) return;
   finalize_split<PRIME>(A);

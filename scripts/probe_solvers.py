@@ -16,11 +16,15 @@ from workloads import make_workload  # noqa: E402
 from workloads.configs import make_custom  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "tiny"
+fit = name.endswith("-fit")          # e.g. large-fit: the library's own poles, as bench.py
+name = name[:-4] if fit else name
 tol = float(sys.argv[2]) if len(sys.argv) > 2 else 1e-10
 solvers = sys.argv[3].split(",") if len(sys.argv) > 3 else ["two_sweep", "split"]
 maxit = int(sys.argv[4]) if len(sys.argv) > 4 else 60000
 wl = make_custom(11, 6, 7, seed=2) if name == "ragged" else make_workload(name)
 table = RationalTable.load(name) if name != "ragged" else RationalTable.load("tiny")
+if fit:
+    table = RationalTable.fit(wl.times, wl.n_poles)
 fw = TemForward(wl.grid.hx, wl.grid.hy, wl.grid.hz)
 sigma = torch.from_numpy(fw.sigma_layout(wl.sigma)).cuda()
 f = torch.from_numpy(fw.source_vector(wl.source)).cuda()
