@@ -6,23 +6,24 @@
 //   tem_synthesize      u(t_k) = sum_s w_s Re(alpha_ks x_s)          (§3.2 eq:rmj, north star (4))
 //   tem_forward_host    all of the above from host buffers
 //
-// Data layout: see include/tem_b200.h.  A shift block keeps the S shifts of
-// one edge contiguous, so a warp's 32 lanes read 32 consecutive complex
-// numbers (512 B, fully coalesced) and every per-edge coefficient (mass,
-// face weights) is loaded once per edge and broadcast to the S lanes that
-// share it: "each coefficient and edge load serves every pole".
+// Data layout: see include/tem_b200.h.  Shift blocks are shift-major
+// ([S][3][Nn] complex): the CTA sweeping one shift streams one contiguous
+// vector, and the S CTAs of one tile run together so every per-edge
+// coefficient (mass) fetched from HBM serves every pole through L2.
 //
-// COCG iteration = three fused sweeps:
-//   k_dir : p = D^-1 r + beta p                               (elementwise)
-//   k_ap  : q = A p on the fly, mu = p^T q                     (stencil + reduction)
-//   k_upd : q = A p again, x += alpha p, r -= alpha q,
-//           z = D^-1 r, rho' = r^T z, ||r||^2                    (stencil + 2 reductions)
-// q is recomputed rather than stored (re-reading p from L2/L1 halo is cheaper
-// than a 16 B/unknown/shift write + read).  Each reduction ends in the last
-// CTA to finish (atomic ticket), which updates the per-shift scalars in
-// device memory; no host round trip per iteration.  The iteration loop is
-// a CUDA graph of `kChunk` iterations; the host checks the active-shift
-// count once per chunk.
+// COCG iteration (both schemes in tem_sweep.cuh):
+//   split (default): k_sweep<3|4>  p = z + beta p_old, q = A p on the fly,
+//                                  z' = z - alpha D^-1 q, (odd) x; gamma, eps,
+//                                  mu, ||r||^2 partials
+//                    k_delta       delta = z'^T A z' by faces -> alpha, beta
+//   two-sweep:       k_sweep<1>    p = z + beta p_old, mu = p^T A p -> alpha
+//                    k_sweep<2>    q = A p again, x, z update -> rho, beta
+// q is recomputed rather than stored (re-reading p through the TMA ring is
+// cheaper than a 16 B/unknown/shift write + read).  Each reduction ends in
+// the last CTA to finish (atomic ticket), which updates the per-shift scalars
+// in device memory; no host round trip per iteration.  The iteration loop is
+// a CUDA graph of `kChunk` iterations; the host checks the active-shift count
+// once per chunk.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -495,49 +496,79 @@ size_t tem_cocg_workspace_bytes(const tem_ctx* c, int S) {
   return work_layout(c, S).total;
 }
 
+// Host side of one batched COCG solve, both schemes (include/tem_b200.h
+// TEM_SOLVER_*).  Per iteration i with parity q = i & 1:
+//   two-sweep: k_sweep<1> (p_new = z + beta p_old in P[1-q], mu = p^T A p ->
+//              alpha) then k_sweep<2> (x, z update; rho, ||r|| -> beta, stop);
+//   split:     pass 1 k_sweep<3> (even i) / k_sweep<4> (odd i): p_i = z_i +
+//              beta p_{i-1}, z_{i+1} = z_i - alpha_i D^-1 A p_i (Z[q] -> Z[1-q],
+//              P[q] -> P[1-q]), odd i also x (R11); partials gamma, eps, mu,
+//              ||r||^2; pass 2 k_delta: delta = z_{i+1}^T A z_{i+1}, the last CTA
+//              forms alpha_{i+1}, beta_{i+1}, the stop test (finalize_split).
+//              Start: k_delta<true> on z_0 (alpha_0 = gamma_0 / delta_0); end:
+//              k_xfix for shifts whose x lags one iteration.
+// Launch configurations depend on the active-slot count (and with it the
+// z-chunking); each is captured once as a CUDA graph of kChunk iterations.
+// The host reads the active count once per graph.
 static int finish_solve(tem_ctx* c, int S, std::vector<tem::ShiftState>& st, const tem::ShiftState* dev_st,
                         cudaEvent_t ev0, cudaEvent_t ev1, cudaStream_t stream, long long launches, int grid,
-                        int block, int* iters, double* relres);
+                        int block, int* iters, double* relres) {
+  TEM_CUDA(cudaMemcpyAsync(st.data(), dev_st, sizeof(tem::ShiftState) * S, cudaMemcpyDeviceToHost, stream));
+  TEM_CUDA(cudaStreamSynchronize(stream));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ev0, ev1);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
 
-static int solve_split(tem_ctx* c, const double* mass, const double* f, int S, const double* shifts,
-                       double tol, int maxit, double* x, char* w, const WorkLayout& L, int* iters,
-                       double* relres, cudaStream_t stream);
+  long long shift_iters = 0;
+  int max_it = 0;
+  int status = TEM_OK;
+  for (int s = 0; s < S; ++s) {
+    if (iters) iters[s] = st[s].iters;
+    if (relres) relres[s] = st[s].relres;
+    shift_iters += st[s].iters;
+    max_it = std::max(max_it, st[s].iters);
+    if (st[s].status == 2) status = TEM_EBREAKDOWN;
+    else if (st[s].status != 1 && status == TEM_OK) status = TEM_ENOCONV;
+  }
+  c->stats.loop_ms = ms;
+  c->stats.kernel_launches = launches;
+  c->stats.shift_iterations = shift_iters;
+  c->stats.iterations = max_it;
+  c->stats.grid = grid;   // with all shifts active
+  c->stats.block = block;
+  if (status == TEM_EBREAKDOWN) return fail(status, "tem_cocg_solve: COCG breakdown");
+  if (status == TEM_ENOCONV) return fail(status, "tem_cocg_solve: not converged within maxit");
+  return TEM_OK;
+}
 
-int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const double* shifts,
-                   double tol, int maxit, double* x, void* work, size_t work_bytes, int* iters,
-                   double* relres, void* stream_) {
-  if (!c || !mass || !f || !shifts || !x || !work) return fail(TEM_EINVAL, "tem_cocg_solve: null pointer");
-  if (int rc = check_S(S)) return rc;
-  if (!(tol > 0.0) || maxit < 1) return fail(TEM_EINVAL, "tem_cocg_solve: need tol > 0, maxit >= 1");
-  const WorkLayout L = work_layout(c, S);
-  if (work_bytes < L.total) return fail(TEM_EINVAL, "tem_cocg_solve: workspace too small");
-  cudaStream_t stream = (cudaStream_t)stream_;
-  if (c->solver == TEM_SOLVER_SPLIT)
-    return solve_split(c, mass, f, S, shifts, tol, maxit, x, static_cast<char*>(work), L, iters, relres,
-                       stream);
-
-  char* w = static_cast<char*>(work);
-
+static int solve(tem_ctx* c, const double* mass, const double* f, int S, const double* shifts, double tol,
+                 int maxit, double* x, char* w, const WorkLayout& L, int* iters, double* relres,
+                 cudaStream_t stream) {
+  const bool split = c->solver == TEM_SOLVER_SPLIT;
+  double2* Z[2] = {reinterpret_cast<double2*>(w + L.z), reinterpret_cast<double2*>(w + L.z1)};
+  double2* P[2] = {reinterpret_cast<double2*>(w + L.p0), reinterpret_cast<double2*>(w + L.p1)};
+  CUtensorMap tmZ[2], tmP[2];
+  for (int q = 0; q < 2; ++q) {
+    if (int rc = make_tmap(c, S, Z[q], &tmZ[q])) return rc;
+    if (int rc = make_tmap(c, S, P[q], &tmP[q])) return rc;
+  }
   tem::SweepArgs base{};
   int grid = 0;
   sweep_geometry(c, S, S, base, &grid);
   base.mass = mass;
   base.x = reinterpret_cast<double2*>(x);
-  base.z = reinterpret_cast<double2*>(w + L.z);
+  base.z = Z[0];
   base.st = reinterpret_cast<tem::ShiftState*>(w + L.st);
   base.ctl = reinterpret_cast<tem::Control*>(w + L.ctl);
   base.part_c = reinterpret_cast<double2*>(w + L.part_c);
   base.part_r = reinterpret_cast<double*>(w + L.part_r);
-  double2* P[2] = {reinterpret_cast<double2*>(w + L.p0), reinterpret_cast<double2*>(w + L.p1)};
-  CUtensorMap tmP[2], tmZ;
-  for (int q = 0; q < 2; ++q)
-    if (int rc = make_tmap(c, S, P[q], &tmP[q])) return rc;
-  if (int rc = make_tmap(c, S, base.z, &tmZ)) return rc;
+  base.part = reinterpret_cast<double*>(w + L.part9);
+  base.pstride = (int)L.nparts;
+  if (const char* env = getenv("TEM_XDIRECT")) base.force_xdirect = atoi(env);   // tests
 
-  // iteration parity q: sweep 1 reads p_old = P[q], writes p_new = P[1-q];
-  // sweep 2 reads P[1-q].  Launch configuration for `nslot` active shifts.
   struct Cfg {
-    tem::SweepArgs a1[2], a2[2];
+    tem::SweepArgs a1[2], a2[2];   // first / second kernel of an iteration, per parity
     int grid;
   };
   auto make_cfg = [&](int nslot) {
@@ -547,16 +578,29 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
     for (int q = 0; q < 2; ++q) {
       k.a1[q] = g0;
       k.a1[q].out = P[1 - q];
+      if (split) {
+        k.a1[q].zin = Z[q];
+        k.a1[q].z = Z[1 - q];
+        k.a1[q].pold = P[q];
+      }
       k.a2[q] = g0;
     }
     return k;
   };
   auto launch_iter = [&](const Cfg& k, int q, cudaStream_t st_) {
-    tem::k_sweep<1><<<k.grid, tem::NT, tem::kSmemDirap, st_>>>(k.a1[q], tmP[q], tmZ);
-    tem::k_sweep<2><<<k.grid, tem::NT, tem::kSmemDirect, st_>>>(k.a2[q], tmP[1 - q], tmP[1 - q]);
+    if (split) {
+      if (q == 0)
+        tem::k_sweep<3><<<k.grid, tem::NT, tem::kSmemDirap, st_>>>(k.a1[0], tmP[0], tmZ[0]);
+      else
+        tem::k_sweep<4><<<k.grid, tem::NT, tem::kSmemDirap, st_>>>(k.a1[1], tmP[1], tmZ[1]);
+      tem::k_delta<false><<<k.grid, tem::NT, tem::kSmemDelta, st_>>>(k.a2[q], tmZ[1 - q]);
+    } else {
+      tem::k_sweep<1><<<k.grid, tem::NT, tem::kSmemDirap, st_>>>(k.a1[q], tmP[q], tmZ[0]);
+      tem::k_sweep<2><<<k.grid, tem::NT, tem::kSmemDirect, st_>>>(k.a2[q], tmP[1 - q], tmP[1 - q]);
+    }
   };
-  // graphs of kChunk iterations, cached per (slots, z-chunks) for these buffers
-  const std::vector<const void*> key = {mass, x, work, f};
+  // graphs of kChunk iterations, cached per (slots, z-chunks) for these buffers and this scheme
+  const std::vector<const void*> key = {mass, x, w, f, reinterpret_cast<const void*>((uintptr_t)c->solver)};
   if (c->graph_key != key || c->graph_S != S) {
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
     c->graphs.clear();
@@ -598,193 +642,17 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
   TEM_CUDA(cudaEventCreate(&ev0));
   TEM_CUDA(cudaEventCreate(&ev1));
   TEM_CUDA(cudaEventRecord(ev0, stream));
-  const int init_grid = S * std::max(1, std::min(64, (int)((3 * c->g.Nn + 255) / 256)));
-  k_init<<<init_grid, 256, 0, stream>>>(base, P[0], P[1], nullptr, f);
+  const int vec_grid = S * std::max(1, std::min(64, (int)((3 * c->g.Nn + 255) / 256)));
+  k_init<<<vec_grid, 256, 0, stream>>>(base, P[0], P[1], split ? Z[1] : nullptr, f);
   TEM_CUDA(cudaGetLastError());
   long long launches = 1;
-
-  const bool trace = getenv("TEM_TRACE") != nullptr;
-  auto t_prev = std::chrono::steady_clock::now();
-  int done = 0;
-  int n_active = S;
   int nslot = S;
   Cfg cfg = make_cfg(nslot);
-  cudaGraphExec_t graph = nullptr;
-  if (int rc = get_graph(cfg, nslot, &graph)) return rc;
-  while (done < maxit) {
-    const int chunk = std::min(kChunk, maxit - done);
-    if (chunk == kChunk) {  // kChunk is even: parity returns to 0
-      TEM_CUDA(cudaGraphLaunch(graph, stream));
-    } else {
-      for (int i = 0; i < chunk; ++i) launch_iter(cfg, (done + i) & 1, stream);
-      TEM_CUDA(cudaGetLastError());
-    }
-    launches += 2LL * chunk;
-    done += chunk;
-    TEM_CUDA(cudaMemcpyAsync(c->pinned_active, &base.ctl->n_active, sizeof(int), cudaMemcpyDeviceToHost, stream));
-    TEM_CUDA(cudaStreamSynchronize(stream));
-    n_active = *c->pinned_active;
-    if (trace) {
-      const auto now = std::chrono::steady_clock::now();
-      fprintf(stderr, "[tem trace] it=%d slots=%d nzc=%d grid=%d active=%d chunk_ms=%.3f\n", done, nslot,
-              cfg.a1[0].nzc, cfg.grid, n_active,
-              std::chrono::duration<double, std::milli>(now - t_prev).count());
-      t_prev = now;
-    }
-    if (n_active == 0) break;
-    if (n_active < nslot) {  // shifts converged: fewer slots, possibly more z-chunks
-      nslot = n_active;
-      cfg = make_cfg(nslot);
-      if (int rc = get_graph(cfg, nslot, &graph)) return rc;
-    }
-  }
-  TEM_CUDA(cudaEventRecord(ev1, stream));
-  return finish_solve(c, S, st, base.st, ev0, ev1, stream, launches, grid, tem::NT, iters, relres);
-}
-
-static int finish_solve(tem_ctx* c, int S, std::vector<tem::ShiftState>& st, const tem::ShiftState* dev_st,
-                        cudaEvent_t ev0, cudaEvent_t ev1, cudaStream_t stream, long long launches, int grid,
-                        int block, int* iters, double* relres) {
-  TEM_CUDA(cudaMemcpyAsync(st.data(), dev_st, sizeof(tem::ShiftState) * S, cudaMemcpyDeviceToHost, stream));
-  TEM_CUDA(cudaStreamSynchronize(stream));
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, ev0, ev1);
-  cudaEventDestroy(ev0);
-  cudaEventDestroy(ev1);
-
-  long long shift_iters = 0;
-  int max_it = 0;
-  int status = TEM_OK;
-  for (int s = 0; s < S; ++s) {
-    if (iters) iters[s] = st[s].iters;
-    if (relres) relres[s] = st[s].relres;
-    shift_iters += st[s].iters;
-    max_it = std::max(max_it, st[s].iters);
-    if (st[s].status == 2) status = TEM_EBREAKDOWN;
-    else if (st[s].status != 1 && status == TEM_OK) status = TEM_ENOCONV;
-  }
-  c->stats.loop_ms = ms;
-  c->stats.kernel_launches = launches;
-  c->stats.shift_iterations = shift_iters;
-  c->stats.iterations = max_it;
-  c->stats.grid = grid;   // with all shifts active
-  c->stats.block = block;
-  if (status == TEM_EBREAKDOWN) return fail(status, "tem_cocg_solve: COCG breakdown");
-  if (status == TEM_ENOCONV) return fail(status, "tem_cocg_solve: not converged within maxit");
-  return TEM_OK;
-}
-
-// Split COCG (tem_sweep.cuh MODE 3/4 + k_delta): per iteration i
-//   pass 1 (k_sweep<3> for even i, <4> for odd i): p_i = z_i + beta p_{i-1},
-//     z_{i+1} = z_i - alpha_i D^-1 A p_i, odd i also x_{i+1} = x_{i-1} +
-//     alpha_{i-1} p_{i-1} + alpha_i p_i; partials gamma, eps, mu, ||r||^2
-//   pass 2 (k_delta): delta = z_{i+1}^T A z_{i+1} by faces; the last CTA
-//     forms alpha_{i+1}, beta_{i+1} and the active list (finalize_split).
-// z and p ping-pong: pass 1 with parity q = i & 1 reads Z[q], P[q] and writes
-// Z[1-q], P[1-q]; pass 2 reads Z[1-q].  Start: k_init, then k_delta<true> on z_0
-// (alpha_0 = gamma_0 / delta_0).  End: k_xfix for shifts whose x lags.
-static int solve_split(tem_ctx* c, const double* mass, const double* f, int S, const double* shifts,
-                       double tol, int maxit, double* x, char* w, const WorkLayout& L, int* iters,
-                       double* relres, cudaStream_t stream) {
-  double2* Z[2] = {reinterpret_cast<double2*>(w + L.z), reinterpret_cast<double2*>(w + L.z1)};
-  double2* P[2] = {reinterpret_cast<double2*>(w + L.p0), reinterpret_cast<double2*>(w + L.p1)};
-  CUtensorMap tmZ[2], tmP[2];
-  for (int q = 0; q < 2; ++q) {
-    if (int rc = make_tmap(c, S, Z[q], &tmZ[q])) return rc;
-    if (int rc = make_tmap(c, S, P[q], &tmP[q])) return rc;
-  }
-  tem::SweepArgs base{};
-  int grid = 0;
-  sweep_geometry(c, S, S, base, &grid);
-  base.mass = mass;
-  base.x = reinterpret_cast<double2*>(x);
-  base.st = reinterpret_cast<tem::ShiftState*>(w + L.st);
-  base.ctl = reinterpret_cast<tem::Control*>(w + L.ctl);
-  base.part_c = reinterpret_cast<double2*>(w + L.part_c);
-  base.part_r = reinterpret_cast<double*>(w + L.part_r);
-  base.part = reinterpret_cast<double*>(w + L.part9);
-  base.pstride = (int)L.nparts;
-  if (const char* env = getenv("TEM_XDIRECT")) base.force_xdirect = atoi(env);   // tests
-
-  struct Cfg {
-    tem::SweepArgs a1[2], a2[2];
-    int grid;
-  };
-  auto make_cfg = [&](int nslot) {
-    Cfg k{};
-    tem::SweepArgs g0 = base;
-    sweep_geometry(c, S, nslot, g0, &k.grid);
-    for (int q = 0; q < 2; ++q) {
-      k.a1[q] = g0;
-      k.a1[q].zin = Z[q];
-      k.a1[q].z = Z[1 - q];
-      k.a1[q].out = P[1 - q];
-      k.a1[q].pold = P[q];
-      k.a2[q] = g0;
-    }
-    return k;
-  };
-  const size_t smem1 = tem::kSmemDirap, smem2 = tem::kSmemDelta;
-  auto launch_iter = [&](const Cfg& k, int q, cudaStream_t st_) {
-    if (q == 0)
-      tem::k_sweep<3><<<k.grid, tem::NT, smem1, st_>>>(k.a1[0], tmP[0], tmZ[0]);
-    else
-      tem::k_sweep<4><<<k.grid, tem::NT, smem1, st_>>>(k.a1[1], tmP[1], tmZ[1]);
-    tem::k_delta<false><<<k.grid, tem::NT, smem2, st_>>>(k.a2[q], tmZ[1 - q]);
-  };
-  const std::vector<const void*> key = {mass, x, w, f, (const void*)2};
-  if (c->graph_key != key || c->graph_S != S) {
-    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
-    c->graphs.clear();
-    c->graph_key = key;
-    c->graph_S = S;
-  }
-  auto get_graph = [&](const Cfg& k, int nslot, cudaGraphExec_t* out) -> int {
-    const long long id = (long long)nslot * 4096 + k.a1[0].nzc;
-    auto it = c->graphs.find(id);
-    if (it != c->graphs.end()) {
-      *out = it->second;
-      return TEM_OK;
-    }
-    cudaGraph_t gr;
-    TEM_CUDA(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
-    for (int i = 0; i < kChunk; ++i) launch_iter(k, i & 1, c->cap_stream);
-    TEM_CUDA(cudaStreamEndCapture(c->cap_stream, &gr));
-    cudaGraphExec_t ex;
-    cudaError_t e = cudaGraphInstantiate(&ex, gr, 0);
-    cudaGraphDestroy(gr);
-    if (e != cudaSuccess) return fail(TEM_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
-    c->graphs[id] = ex;
-    *out = ex;
-    return TEM_OK;
-  };
-
-  std::vector<tem::ShiftState> st(S);
-  for (int s = 0; s < S; ++s) {
-    memset(&st[s], 0, sizeof(tem::ShiftState));
-    st[s].s = make_double2(shifts[2 * s], shifts[2 * s + 1]);
-  }
-  tem::Control ctl{};
-  ctl.tol = tol;
-  TEM_CUDA(cudaMemcpyAsync(base.st, st.data(), sizeof(tem::ShiftState) * S, cudaMemcpyHostToDevice, stream));
-  TEM_CUDA(cudaMemcpyAsync(base.ctl, &ctl, sizeof(tem::Control), cudaMemcpyHostToDevice, stream));
-
-  cudaEvent_t ev0, ev1;
-  TEM_CUDA(cudaEventCreate(&ev0));
-  TEM_CUDA(cudaEventCreate(&ev1));
-  TEM_CUDA(cudaEventRecord(ev0, stream));
-  {
-    tem::SweepArgs ia = base;
-    ia.z = Z[0];
-    const int init_grid = S * std::max(1, std::min(64, (int)((3 * c->g.Nn + 255) / 256)));
-    k_init<<<init_grid, 256, 0, stream>>>(ia, P[0], P[1], Z[1], f);
+  if (split) {
+    tem::k_delta<true><<<cfg.grid, tem::NT, tem::kSmemDelta, stream>>>(cfg.a2[0], tmZ[0]);   // delta_0
     TEM_CUDA(cudaGetLastError());
+    launches += 1;
   }
-  int nslot = S;
-  Cfg cfg = make_cfg(nslot);
-  tem::k_delta<true><<<cfg.grid, tem::NT, smem2, stream>>>(cfg.a2[0], tmZ[0]);   // delta_0
-  TEM_CUDA(cudaGetLastError());
-  long long launches = 2;
 
   const bool trace = getenv("TEM_TRACE") != nullptr;
   auto t_prev = std::chrono::steady_clock::now();
@@ -812,20 +680,31 @@ static int solve_split(tem_ctx* c, const double* mass, const double* f, int S, c
       t_prev = now;
     }
     if (n_active == 0) break;
-    if (n_active < nslot) {
+    if (n_active < nslot) {  // shifts converged: fewer slots, possibly more z-chunks
       nslot = n_active;
       cfg = make_cfg(nslot);
       if (int rc = get_graph(cfg, nslot, &graph)) return rc;
     }
   }
-  {
-    const int fix_grid = S * std::max(1, std::min(64, (int)((3 * c->g.Nn + 255) / 256)));
-    k_xfix<<<fix_grid, 256, 0, stream>>>(base, P[1]);
+  if (split) {
+    k_xfix<<<vec_grid, 256, 0, stream>>>(base, P[1]);
     TEM_CUDA(cudaGetLastError());
     launches += 1;
   }
   TEM_CUDA(cudaEventRecord(ev1, stream));
   return finish_solve(c, S, st, base.st, ev0, ev1, stream, launches, grid, tem::NT, iters, relres);
+}
+
+int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const double* shifts,
+                   double tol, int maxit, double* x, void* work, size_t work_bytes, int* iters,
+                   double* relres, void* stream_) {
+  if (!c || !mass || !f || !shifts || !x || !work) return fail(TEM_EINVAL, "tem_cocg_solve: null pointer");
+  if (int rc = check_S(S)) return rc;
+  if (!(tol > 0.0) || maxit < 1) return fail(TEM_EINVAL, "tem_cocg_solve: need tol > 0, maxit >= 1");
+  const WorkLayout L = work_layout(c, S);
+  if (work_bytes < L.total) return fail(TEM_EINVAL, "tem_cocg_solve: workspace too small");
+  return solve(c, mass, f, S, shifts, tol, maxit, x, static_cast<char*>(work), L, iters, relres,
+               (cudaStream_t)stream_);
 }
 
 int tem_set_solver(tem_ctx* c, int solver) {
