@@ -16,9 +16,14 @@ roofline: the COCG sweep kernels against measured HBM bandwidth, at the
           algorithmic 128 B per shift-unknown-iteration.
 e2e     : the same step through tem_forward_host with pinned HOST buffers
           (sigma, f uploaded; all channel fields downloaded) each step.
-N > 1   : one process per GPU (torchrun), each rank an independent
-          sounding (the transmitter moved by rank) -> weak scaling, no
-          data-path collective.
+N > 1   : one process per GPU (torchrun).  Default --partition soundings:
+          each rank an independent sounding (the transmitter moved by rank)
+          -> weak scaling, no data-path collective.  --partition shifts: ONE
+          sounding, its shifted systems dealt to the ranks
+          (paper_2506_11657_b200.distributed), each rank synthesises its
+          partial sum of every channel and one NCCL reduce sums them onto
+          rank 0 inside the timed step -> strong scaling (DESIGN.md
+          "Multi-GPU").
 """
 from __future__ import annotations
 
@@ -164,8 +169,11 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
-    wl = _workload_for_rank(args.config, rank)
+    from paper_2506_11657_b200.distributed import forward_partial, reduce_channels, shard_shifts
+    by_shift = args.partition == "shifts"
+    wl = _workload_for_rank(args.config, 0 if by_shift else rank)
     table = _poles(args, wl)
+    idx = shard_shifts(table.shifts, ws)[rank] if by_shift else np.arange(table.n_shift)
     fw = TemForward(wl.grid.hx, wl.grid.hy, wl.grid.hz, device=dev)
     if args.solver:
         fw.solver = args.solver
@@ -177,10 +185,11 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        mass = fw.edge_mass(sigma)
-        x, iters, relres = fw.cocg(mass, f, table.shifts, tol=args.tol, maxit=args.maxit)
-        u = fw.synthesize(x, table.residues, table.is_pair)
-        st = fw.stats()
+        u, iters, relres = forward_partial(fw, sigma, f, table, idx, tol=args.tol, maxit=args.maxit)
+        if by_shift:
+            reduce_channels(u, dst=0)            # the one exchange: sum of partial channels
+        st = fw.stats() if len(idx) else {"shift_iterations": 0, "loop_ms": 0.0,
+                                          "kernel_launches": 0, "iterations": 0}
         return u, iters, relres, st
 
     def barrier():
@@ -204,7 +213,7 @@ def run_ours(args):
             u, iters, relres, st = step()
             sui += int(st["shift_iterations"]) * N
             loop_ms += st["loop_ms"]
-            launches += int(st["kernel_launches"]) + 2      # + edge mass + synthesis
+            launches += int(st["kernel_launches"]) + (2 if len(idx) else 0)   # + edge mass + synthesis
             del u
         e1.record(stream)
         barrier()
@@ -216,7 +225,32 @@ def run_ours(args):
 
     # ---- e2e through the C ABI with pinned host buffers (rank-local, then max)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and by_shift:
+        # host sigma, f up; partial forward; reduce; u down on rank 0
+        sig_h = torch.from_numpy(fw.sigma_layout(wl.sigma)).pin_memory()
+        f_h = torch.from_numpy(fw.source_vector(wl.source)).pin_memory()
+        u_h = torch.empty((K, fw.n_slots), dtype=torch.float64).pin_memory()
+        barrier()
+        t0 = time.perf_counter()
+        e2e_sui = 0
+        for _ in range(args.steps):
+            sig_d = sig_h.to(dev, non_blocking=True)
+            f_d = f_h.to(dev, non_blocking=True)
+            u, it_h, _ = forward_partial(fw, sig_d, f_d, table, idx, tol=args.tol, maxit=args.maxit)
+            reduce_channels(u, dst=0)
+            if rank == 0:
+                u_h.copy_(u)
+            torch.cuda.synchronize(dev)
+            e2e_sui += int(np.sum(it_h)) * N
+        barrier()
+        e2e_s = time.perf_counter() - t0
+        (e2e_s,), (e2e_sui,) = reduce_job([e2e_s], [e2e_sui], dev)
+        e2e = {"value": e2e_sui / e2e_s, "unit": "shift-unknown-iterations/s",
+               "h2d_bytes_per_step": int(sig_h.numel() * 8 + f_h.numel() * 8),
+               "d2h_bytes_per_step": int(u_h.numel() * 8),
+               "ms_per_step": 1e3 * e2e_s / args.steps}
+        del u_h
+    elif not args.no_e2e:
         sig_h = torch.from_numpy(fw.sigma_layout(wl.sigma)).pin_memory()
         f_h = torch.from_numpy(fw.source_vector(wl.source)).pin_memory()
         u_h = torch.empty((K, fw.n_slots), dtype=torch.float64).pin_memory()
@@ -265,7 +299,7 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": t_max / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if by_shift else "weak",
         "vs_baseline": None,
         "dtype": "c128",
         "data": "synthetic (seeded earth model, BASELINE configs[4] shape)",
@@ -276,7 +310,9 @@ def run_ours(args):
                    "iterations_per_shift": [int(i) for i in iters],
                    "l2": "inputs larger than L2 (each shift block %.2f GB)" % (fw.n_slots * S * 16 / 1e9),
                    "wall_time_to_all_channels_ms": t_max / args.steps,
-                   "parallelism": f"{ws} independent soundings" if ws > 1 else "1 GPU"},
+                   "parallelism": (f"{ws} ranks x shifts {[len(p) for p in shard_shifts(table.shifts, ws)]}"
+                                   ", NCCL reduce of the channel fields" if by_shift and ws > 1 else
+                                   f"{ws} independent soundings" if ws > 1 else "1 GPU")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "traffic_unit": "DRAM bytes per COCG iteration (all sweeps, all shifts active; "
@@ -359,6 +395,9 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=8)
     ap.add_argument("--solver", default=None, choices=["split", "two_sweep"],
                     help="COCG scheme (default: the library's, tem_get_solver)")
+    ap.add_argument("--partition", default="soundings", choices=["soundings", "shifts"],
+                    help="N>1: independent soundings per rank (weak) or one sounding's shifts "
+                         "over the ranks + NCCL reduce of the channels (strong)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -65,3 +65,55 @@ def test_rank_soundings_valid_and_distinct(name):
         for (c, i, j, k, s) in wl.source:
             assert 1 <= j <= ny - 1 and k == wl.surface_k
             assert 0 <= i < nx
+
+
+# ---------------------------------------------------------------- shift partition
+@pytest.mark.parametrize("S,world", [(14, 1), (14, 2), (14, 4), (12, 8), (3, 8), (32, 8)])
+def test_shard_shifts_is_a_balanced_partition(S, world):
+    from paper_2506_11657_b200.distributed import shard_shifts
+    rng = np.random.default_rng(S + world)
+    shifts = (10 ** rng.uniform(2, 6, S)) * np.exp(1j * rng.uniform(-1.5, 1.5, S))
+    parts = shard_shifts(shifts, world)
+    assert len(parts) == world
+    allidx = np.sort(np.concatenate(parts))
+    assert np.array_equal(allidx, np.arange(S))                    # every shift exactly once
+    sizes = [len(p) for p in parts]
+    assert max(sizes) - min(sizes) <= 1                             # balanced counts
+    if S >= 2 * world:                                              # snake: each rank gets hard and easy
+        order = np.argsort(np.abs(shifts))
+        hardest = set(order[:world].tolist())
+        assert all(len(hardest & set(p.tolist())) == 1 for p in parts)
+
+
+def _reduce_worker(rank, world, port, out):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    from oracle import forward as ofw
+    from paper_2506_11657_b200 import RationalTable
+    from paper_2506_11657_b200.distributed import reduce_channels, shard_shifts
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    table = RationalTable.load("tiny")
+    rng = np.random.default_rng(5)
+    X = rng.normal(size=(300, table.n_shift)) + 1j * rng.normal(size=(300, table.n_shift))
+    idx = shard_shifts(table.shifts, world)[rank]
+    # this rank's partial channel fields (the oracle's synthesis stands in for k_synth)
+    up = ofw.synthesize(X[:, idx], table.residues[idx], table.is_pair[idx]).T.copy()
+    u = reduce_channels(torch.from_numpy(up), dst=0)
+    if rank == 0:
+        full = ofw.synthesize(X, table.residues, table.is_pair).T
+        out["err"] = float(np.abs(u.numpy() - full).max() / np.abs(full).max())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shift_partitioned_channels_reduce_to_the_full_sum_gloo(world):
+    """--partition shifts: per-rank partial sums of eq:rmj over the rank's
+    shifts, one reduce -> the full channel fields on rank 0."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_reduce_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    assert out["err"] <= 1e-14
