@@ -257,7 +257,8 @@ struct tem_ctx {
   size_t e2e_bytes = 0;
   // stats of the last solve
   tem_solve_stats stats{};
-  int sweep_per_sm = 2;             // resident sweep CTAs per SM (occupancy of k_sweep<1>)
+  int per_sm_two = 2;               // resident CTAs per SM of k_sweep<1> (two-sweep geometry)
+  int per_sm_split = 1;             // resident CTAs per SM of k_sweep<3> (split geometry)
   int solver = TEM_SOLVER_SPLIT;
   int band = 4;                     // tile rows per band of the sweep block order (block_coords)
 };
@@ -270,17 +271,20 @@ static int check_S(int S) {
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-// sweep geometry: xy tiles x z-chunks x shift slots.  The z-range is split
-// until the grid covers ~4 waves of 2 CTAs/SM, so that a few remaining
+// sweep geometry of one scheme: xy tiles x z-chunks x shift slots, for tile
+// height ty (tem::kTYTwoSweep or tem::kTYSplit).  The z-range is split until
+// the grid covers ~4 waves of resident CTAs, so that a few remaining
 // (slow-converging) shifts still fill the machine.
-static void sweep_geometry(const tem_ctx* c, int S, int nslot, tem::SweepArgs& A, int* grid) {
+static void sweep_geometry(const tem_ctx* c, int S, int nslot, tem::SweepArgs& A, int* grid,
+                           int ty = tem::kTYTwoSweep) {
   A.g = c->g;
   A.S = S;
   A.nslot = nslot;
   A.band = c->band;
-  A.ntx = (c->g.n[0] + tem::TX - 1) / tem::TX;
-  A.nty = (c->g.n[1] + tem::TY - 1) / tem::TY;
-  const int target = 4 * c->num_sms * c->sweep_per_sm;
+  A.ntx = (c->g.n[0] + 32 - 1) / 32;
+  A.nty = (c->g.n[1] + ty - 1) / ty;
+  const int per_sm = ty == tem::kTYSplit ? c->per_sm_split : c->per_sm_two;
+  const int target = 4 * c->num_sms * per_sm;
   const int base = A.ntx * A.nty * nslot;
   int nzc = 1;
   while (base * nzc < target && c->g.n[2] / (nzc * 2) >= 16) nzc *= 2;
@@ -293,33 +297,37 @@ static void sweep_geometry(const tem_ctx* c, int S, int nslot, tem::SweepArgs& A
 
 static int max_sweep_grid(const tem_ctx* c, int S) {
   int gmax = 0;
-  for (int ns = 1; ns <= S; ++ns) {
-    tem::SweepArgs A{};
-    int gr = 0;
-    sweep_geometry(c, S, ns, A, &gr);
-    gmax = std::max(gmax, gr);
-  }
+  for (int ty : {tem::kTYTwoSweep, tem::kTYSplit})
+    for (int ns = 1; ns <= S; ++ns) {
+      tem::SweepArgs A{};
+      int gr = 0;
+      sweep_geometry(c, S, ns, A, &gr, ty);
+      gmax = std::max(gmax, gr);
+    }
   return gmax;
 }
 
 static int sweep_attrs() {
   static bool done = false;
   if (done) return TEM_OK;
-  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmemDirect));
-  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmemDirect));
-  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmemDirap));
-  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmemDirap));
-  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmemDirap));
-  TEM_CUDA(cudaFuncSetAttribute(tem::k_delta<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmemDelta));
-  TEM_CUDA(cudaFuncSetAttribute(tem::k_delta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tem::kSmemDelta));
+  using T2 = tem::Tile<tem::kTYTwoSweep>;
+  using TS = tem::Tile<tem::kTYSplit>;
+  const int attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<0>, (cudaFuncAttribute)attr, (int)T2::kSmemDirect));
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<2>, (cudaFuncAttribute)attr, (int)T2::kSmemDirect));
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<1>, (cudaFuncAttribute)attr, (int)T2::kSmemDirap));
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<3>, (cudaFuncAttribute)attr, (int)TS::kSmemDirap));
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<4>, (cudaFuncAttribute)attr, (int)TS::kSmemDirap));
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_delta<false>, (cudaFuncAttribute)attr, (int)TS::kSmemDelta));
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_delta<true>, (cudaFuncAttribute)attr, (int)TS::kSmemDelta));
   done = true;
   return TEM_OK;
 }
 
 // 5-D tiled tensor map over a shift block [S][3][nz+1][ny+1][nx+1] complex
 // fp64 (as 2(nx+1) doubles innermost); box = one halo-extended plane tile.
-static int make_tmap(const tem_ctx* c, int S, const void* base, CUtensorMap* tm,
-                     int box_x = tem::HX, int box_y = tem::HY) {
+static int make_tmap(const tem_ctx* c, int S, const void* base, CUtensorMap* tm, int ty = tem::kTYTwoSweep) {
+  const int box_x = 32 + 2, box_y = ty + 2;   // halo-extended plane tile (Tile<ty>::HX, HY)
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -412,8 +420,12 @@ int tem_create(int nx, int ny, int nz, const double* hx, const double* hy, const
   if (const char* env = getenv("TEM_BAND")) c->band = atoi(env);   // experiments
   {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tem::k_sweep<1>, tem::NT, tem::kSmemDirap);
-    c->sweep_per_sm = std::max(1, per_sm);
+    using T2 = tem::Tile<tem::kTYTwoSweep>;
+    using TS = tem::Tile<tem::kTYSplit>;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tem::k_sweep<1>, T2::NT, T2::kSmemDirap);
+    c->per_sm_two = std::max(1, per_sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tem::k_sweep<3>, TS::NT, TS::kSmemDirap);
+    c->per_sm_split = std::max(1, per_sm);
   }
   *out = c;
   return TEM_OK;
@@ -461,7 +473,8 @@ int tem_apply_shifted(tem_ctx* c, const double* mass, int S, const double* shift
   CUtensorMap tm;
   if (int rc = make_tmap(c, S, x, &tm)) return rc;
   TEM_CUDA(cudaMemsetAsync(y, 0, (size_t)3 * c->g.Nn * S * sizeof(double2), (cudaStream_t)stream));
-  tem::k_sweep<0><<<grid, tem::NT, tem::kSmemDirect, (cudaStream_t)stream>>>(A, tm, tm);
+  using T2 = tem::Tile<tem::kTYTwoSweep>;
+  tem::k_sweep<0><<<grid, T2::NT, T2::kSmemDirect, (cudaStream_t)stream>>>(A, tm, tm);
   TEM_CUDA(cudaGetLastError());
   return TEM_OK;
 }
@@ -546,16 +559,20 @@ static int solve(tem_ctx* c, const double* mass, const double* f, int S, const d
                  int maxit, double* x, char* w, const WorkLayout& L, int* iters, double* relres,
                  cudaStream_t stream) {
   const bool split = c->solver == TEM_SOLVER_SPLIT;
+  using T2 = tem::Tile<tem::kTYTwoSweep>;
+  using TS = tem::Tile<tem::kTYSplit>;
+  const int ty = split ? tem::kTYSplit : tem::kTYTwoSweep;
+  const int nt = split ? TS::NT : T2::NT;
   double2* Z[2] = {reinterpret_cast<double2*>(w + L.z), reinterpret_cast<double2*>(w + L.z1)};
   double2* P[2] = {reinterpret_cast<double2*>(w + L.p0), reinterpret_cast<double2*>(w + L.p1)};
   CUtensorMap tmZ[2], tmP[2];
   for (int q = 0; q < 2; ++q) {
-    if (int rc = make_tmap(c, S, Z[q], &tmZ[q])) return rc;
-    if (int rc = make_tmap(c, S, P[q], &tmP[q])) return rc;
+    if (int rc = make_tmap(c, S, Z[q], &tmZ[q], ty)) return rc;
+    if (int rc = make_tmap(c, S, P[q], &tmP[q], ty)) return rc;
   }
   tem::SweepArgs base{};
   int grid = 0;
-  sweep_geometry(c, S, S, base, &grid);
+  sweep_geometry(c, S, S, base, &grid, ty);
   base.mass = mass;
   base.x = reinterpret_cast<double2*>(x);
   base.z = Z[0];
@@ -574,7 +591,7 @@ static int solve(tem_ctx* c, const double* mass, const double* f, int S, const d
   auto make_cfg = [&](int nslot) {
     Cfg k{};
     tem::SweepArgs g0 = base;
-    sweep_geometry(c, S, nslot, g0, &k.grid);
+    sweep_geometry(c, S, nslot, g0, &k.grid, ty);
     for (int q = 0; q < 2; ++q) {
       k.a1[q] = g0;
       k.a1[q].out = P[1 - q];
@@ -590,13 +607,13 @@ static int solve(tem_ctx* c, const double* mass, const double* f, int S, const d
   auto launch_iter = [&](const Cfg& k, int q, cudaStream_t st_) {
     if (split) {
       if (q == 0)
-        tem::k_sweep<3><<<k.grid, tem::NT, tem::kSmemDirap, st_>>>(k.a1[0], tmP[0], tmZ[0]);
+        tem::k_sweep<3><<<k.grid, TS::NT, TS::kSmemDirap, st_>>>(k.a1[0], tmP[0], tmZ[0]);
       else
-        tem::k_sweep<4><<<k.grid, tem::NT, tem::kSmemDirap, st_>>>(k.a1[1], tmP[1], tmZ[1]);
-      tem::k_delta<false><<<k.grid, tem::NT, tem::kSmemDelta, st_>>>(k.a2[q], tmZ[1 - q]);
+        tem::k_sweep<4><<<k.grid, TS::NT, TS::kSmemDirap, st_>>>(k.a1[1], tmP[1], tmZ[1]);
+      tem::k_delta<false><<<k.grid, TS::NT, TS::kSmemDelta, st_>>>(k.a2[q], tmZ[1 - q]);
     } else {
-      tem::k_sweep<1><<<k.grid, tem::NT, tem::kSmemDirap, st_>>>(k.a1[q], tmP[q], tmZ[0]);
-      tem::k_sweep<2><<<k.grid, tem::NT, tem::kSmemDirect, st_>>>(k.a2[q], tmP[1 - q], tmP[1 - q]);
+      tem::k_sweep<1><<<k.grid, T2::NT, T2::kSmemDirap, st_>>>(k.a1[q], tmP[q], tmZ[0]);
+      tem::k_sweep<2><<<k.grid, T2::NT, T2::kSmemDirect, st_>>>(k.a2[q], tmP[1 - q], tmP[1 - q]);
     }
   };
   // graphs of kChunk iterations, cached per (slots, z-chunks) for these buffers and this scheme
@@ -649,7 +666,7 @@ static int solve(tem_ctx* c, const double* mass, const double* f, int S, const d
   int nslot = S;
   Cfg cfg = make_cfg(nslot);
   if (split) {
-    tem::k_delta<true><<<cfg.grid, tem::NT, tem::kSmemDelta, stream>>>(cfg.a2[0], tmZ[0]);   // delta_0
+    tem::k_delta<true><<<cfg.grid, TS::NT, TS::kSmemDelta, stream>>>(cfg.a2[0], tmZ[0]);   // delta_0
     TEM_CUDA(cudaGetLastError());
     launches += 1;
   }
@@ -692,7 +709,7 @@ static int solve(tem_ctx* c, const double* mass, const double* f, int S, const d
     launches += 1;
   }
   TEM_CUDA(cudaEventRecord(ev1, stream));
-  return finish_solve(c, S, st, base.st, ev0, ev1, stream, launches, grid, tem::NT, iters, relres);
+  return finish_solve(c, S, st, base.st, ev0, ev1, stream, launches, grid, nt, iters, relres);
 }
 
 int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const double* shifts,

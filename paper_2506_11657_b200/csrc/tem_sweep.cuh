@@ -28,22 +28,36 @@
 
 namespace tem {
 
-constexpr int TX = 32;                    // tile nodes along x (one warp row)
-#ifndef TEM_TY
-#define TEM_TY 8
-#endif
-constexpr int TY = TEM_TY;                // tile nodes along y (8: 2 CTAs/SM; 16: 1 CTA/SM)
-constexpr int kMinBlocks = TY <= 8 ? 2 : 1;
-constexpr int NT = TX * TY;               // threads per CTA
-constexpr int HX = TX + 2, HY = TY + 2;   // halo-extended tile
-constexpr int TILE_BYTES = HX * HY * 16;  // one plane tile as delivered by TMA (5440 B)
-constexpr int TILE_STRIDE = (TILE_BYTES + 127) / 128 * 128;   // slot pitch (128 B aligned)
-constexpr int TS2 = TILE_STRIDE / 16;     // slot pitch in double2
-
-// ring: sets q = {X(q+1), Y(q+1), Z(q)}; X,Y: 5 slots, Z: 4 slots (+ MODE 1 z staging 2 x 3)
+// Tile geometry, by tile height: a CTA owns TX x TYV nodes (one thread per
+// node).  TYV = 8: 256 threads, 2 CTAs/SM at <= 128 registers (two-sweep
+// scheme, operator apply); TYV = 12: 384 threads, 1 CTA/SM at <= 168
+// registers (split scheme: its pass 1 carries the full update and spills at
+// 128 registers; measured -12% on the odd pass).
+// ring: sets q = {X(q+1), Y(q+1), Z(q)}; X,Y: 5 slots, Z: 4 slots (+ z staging 2 x 3)
 constexpr int R_XY = 5, R_Z = 4;
-constexpr size_t kSmemDirect = 128 + (size_t)(2 * R_XY + R_Z) * TILE_STRIDE;        // 77 KB at TY=8
-constexpr size_t kSmemDirap = kSmemDirect + (size_t)6 * TILE_STRIDE;              // 110 KB at TY=8
+constexpr int R_D = 4;                    // k_delta ring depth (whole plane sets)
+template <int TYV>
+struct Tile {
+  static constexpr int TX = 32;                    // tile nodes along x (one warp row)
+  static constexpr int TY = TYV;
+  static constexpr int NT = TX * TY;               // threads per CTA
+  static constexpr int kMinBlocks = NT <= 256 ? 2 : 1;
+  static constexpr int HX = TX + 2, HY = TY + 2;   // halo-extended tile
+  static constexpr int TILE_BYTES = HX * HY * 16;  // one plane tile as delivered by TMA
+  static constexpr int TILE_STRIDE = (TILE_BYTES + 127) / 128 * 128;   // slot pitch (128 B aligned)
+  static constexpr int TS2 = TILE_STRIDE / 16;     // slot pitch in double2
+  static constexpr size_t kSmemDirect = 128 + (size_t)(2 * R_XY + R_Z) * TILE_STRIDE;
+  static constexpr size_t kSmemDirap = kSmemDirect + (size_t)6 * TILE_STRIDE;
+  static constexpr size_t kSmemDelta = 128 + (size_t)3 * R_D * TILE_STRIDE;
+};
+constexpr int kTYTwoSweep = 8;    // tile height of MODE 0, 1, 2
+constexpr int kTYSplit = 12;      // tile height of MODE 3, 4 and k_delta
+#define TEM_TILE_CONSTANTS(TYV)                                                              \
+  constexpr int TX = Tile<TYV>::TX, TY = Tile<TYV>::TY, NT = Tile<TYV>::NT;                 \
+  constexpr int HX = Tile<TYV>::HX, HY = Tile<TYV>::HY, TS2 = Tile<TYV>::TS2;               \
+  constexpr int TILE_BYTES = Tile<TYV>::TILE_BYTES;                                         \
+  (void)TX; (void)TY; (void)NT; (void)HX; (void)HY; (void)TS2; (void)TILE_BYTES
+
 constexpr int kMaxChunk = 128;            // max planes per z-chunk (z tables in smem)
 
 struct ShiftState {
@@ -237,7 +251,9 @@ __device__ __forceinline__ Column make_column_ij(const Grid& g, int i, int j) {
   return C;
 }
 
+template <int TYV>
 __device__ __forceinline__ Column make_column(const Grid& g, int tx0, int ty0) {
+  TEM_TILE_CONSTANTS(TYV);
   const int tid = threadIdx.x;
   Column C = make_column_ij(g, tx0 + (tid % TX), ty0 + (tid / TX));
   C.c0 = ((tid / TX) + 1) * HX + (tid % TX) + 1;
@@ -309,12 +325,13 @@ __device__ __forceinline__ void stencil3p(const Grid& g, const Column& C, int c0
   E.p[2] = z00;
 }
 
+template <int TYV>
 __device__ __forceinline__ void stencil3(const Grid& g, const Column& C, int k, double ihz, double ihzm,
                                          double hdz, const double2* Xm, const double2* X0,
                                          const double2* Xp, const double2* Ym, const double2* Y0,
                                          const double2* Yp, const double2* Zm, const double2* Z0,
                                          Edge3& E) {
-  stencil3p<HX>(g, C, C.c0, k, ihz, ihzm, hdz, Xm, X0, Xp, Ym, Y0, Yp, Zm, Z0, E);
+  stencil3p<Tile<TYV>::HX>(g, C, C.c0, k, ihz, ihzm, hdz, Xm, X0, Xp, Ym, Y0, Yp, Zm, Z0, E);
 }
 
 // v^T K v restricted to the three faces whose lower corner is this node
@@ -323,9 +340,11 @@ __device__ __forceinline__ void stencil3(const Grid& g, const Column& C, int k, 
 // nodes every face is counted once; it reads only the +x, +y, +z neighbours.
 __device__ __forceinline__ double2 csq(double2 a) { return make_double2(fma(a.x, a.x, -a.y * a.y), 2.0 * a.x * a.y); }
 
+template <int TYV>
 __device__ __forceinline__ double2 faces_quad(const Column& C, double ihz, double hdz, const double2* X0,
                                               const double2* Xp, const double2* Y0, const double2* Yp,
                                               const double2* Z0, double2 v[3]) {
+  constexpr int HX = Tile<TYV>::HX;
   const int c0 = C.c0;
   const double2 x00 = X0[c0], y00 = Y0[c0], z00 = Z0[c0];
   const double2 Fz = csub(cadd(x00, Y0[c0 + 1]), cadd(X0[c0 + HX], y00));
@@ -345,16 +364,15 @@ __device__ __forceinline__ double2 faces_quad(const Column& C, double ihz, doubl
 // shift) with a +1 halo; plane sets q = {X(q), Y(q), Z(q)} in a 4-deep ring
 // (step k reads sets k and k+1, sets k+2 and k+3 in flight): 12 tiles, 66 KB,
 // three CTAs per SM.
-constexpr int R_D = 4;
-constexpr size_t kSmemDelta = 128 + (size_t)3 * R_D * TILE_STRIDE;
 
 // Split solver finalisation (last CTA of pass 2): per-shift sums of the pass-1
 // partials (gamma, eps, mu, ||r||^2) and the pass-2 partial delta, then
 //   beta = gamma / gamma_prev,  p^T A p = delta + beta (2 eps + beta mu),
 //   alpha = gamma / p^T A p     (reading R10)
 // PRIME (after k_init): alpha_0 = gamma_0 / delta_0.
-template <bool PRIME>
+template <bool PRIME, int TYV>
 __device__ void finalize_split(const SweepArgs& A) {
+  constexpr int NT = Tile<TYV>::NT;
   const int S = A.S, ns = A.nslot;
   const int n_list = A.ctl->n_active;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -419,8 +437,9 @@ __device__ void finalize_split(const SweepArgs& A) {
 // Finalisation by the last CTA: per-shift sums of the per-CTA partials (the
 // CTAs of slot a are blockIdx = a mod nslot and served shift list[a]), COCG
 // scalar updates, then the compacted active list for the next launch.
-template <int MODE>
+template <int MODE, int TYV>
 __device__ void finalize(const SweepArgs& A) {
+  constexpr int NT = Tile<TYV>::NT;
   const int S = A.S, ns = A.nslot;
   const int n_list = A.ctl->n_active;   // as read by every CTA of this launch
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -481,8 +500,10 @@ __device__ void finalize(const SweepArgs& A) {
 // neighbour in the band (L2 hits instead of DRAM re-reads).  band = 0: the
 // slot-fastest order (slot, then column, then row).  pidx: index of the
 // block's reduction partials, slot-major ([slot][tile and chunk]).
+template <int TYV>
 __device__ __forceinline__ void block_coords(const SweepArgs& A, int& a, int& tx0, int& ty0, int& kb,
                                              int& ke, int& pidx) {
+  constexpr int TX = Tile<TYV>::TX, TY = Tile<TYV>::TY;
   const int ns = A.nslot, ntx = A.ntx, nty = A.nty;
   const int per_z = ns * ntx * nty;
   const int zc = blockIdx.x / per_z;
@@ -518,10 +539,11 @@ __device__ __forceinline__ void block_coords(const SweepArgs& A, int& a, int& tx
 // staging area; when set q has landed it is combined IN PLACE into
 // p_new = z + beta p_old (at the end of step q-1, two sets ahead), so MODE 1
 // needs 20 tiles (110 KB) and also runs 2 CTAs per SM.
-template <int MODE>
-__global__ void __launch_bounds__(NT, kMinBlocks) k_sweep(const __grid_constant__ SweepArgs A,
-                                                 const __grid_constant__ CUtensorMap tmv,
-                                                 const __grid_constant__ CUtensorMap tmz) {
+template <int MODE, int TYV = (MODE >= 3 ? kTYSplit : kTYTwoSweep)>
+__global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
+    k_sweep(const __grid_constant__ SweepArgs A, const __grid_constant__ CUtensorMap tmv,
+            const __grid_constant__ CUtensorMap tmz) {
+  TEM_TILE_CONSTANTS(TYV);
   constexpr bool kZ = (MODE == 1 || MODE == 3 || MODE == 4);   // p_new = z + beta p_old formed in smem
   constexpr bool kUpd = (MODE == 3 || MODE == 4);               // split pass 1: full update
   extern __shared__ unsigned char smem_raw[];
@@ -538,7 +560,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) k_sweep(const __grid_constant_
   const Grid& g = A.g;
   int a, tx0, ty0, kb, ke;
   int pidx;
-  block_coords(A, a, tx0, ty0, kb, ke, pidx);
+  block_coords<TYV>(A, a, tx0, ty0, kb, ke, pidx);
   const int tid = threadIdx.x;
 
   double2 sh = czero(), alpha = czero(), beta = czero(), alpha_prev = czero();
@@ -573,7 +595,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) k_sweep(const __grid_constant_
   }
 
   if (live) {
-    const Column C = make_column(g, tx0, ty0);
+    const Column C = make_column<TYV>(g, tx0, ty0);
     const long long vs = (long long)s * 3 * g.Nn;
     const int nx1 = g.n[0] + 1, ny1 = g.n[1] + 1;
     for (int q = tid; q <= ke - kb; q += NT) {
@@ -676,7 +698,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) k_sweep(const __grid_constant_
     for (int k = kb; k < ke; ++k) {
       if (!kZ) wait_set(k);
       Edge3 E;
-      stencil3(g, C, k, zih[k - kb + 1], zih[k - kb], zhd[k - kb], rX + sxm * TS2, rX + sx0 * TS2,
+      stencil3<TYV>(g, C, k, zih[k - kb + 1], zih[k - kb], zhd[k - kb], rX + sxm * TS2, rX + sx0 * TS2,
                rX + sxp * TS2, rY + sxm * TS2, rY + sx0 * TS2, rY + sxp * TS2, rZ + szm * TS2,
                rZ + sz0 * TS2, E);
       sxm = sx0;
@@ -757,16 +779,17 @@ __global__ void __launch_bounds__(NT, kMinBlocks) k_sweep(const __grid_constant_
     A.part_r[pidx] = acc_r;
   }
   if (!last_block(&A.ctl->ticket[MODE])) return;
-  finalize<MODE>(A);
+  finalize<MODE, TYV>(A);
 }
 
 }  // namespace tem
 
 namespace tem {
 
-template <bool PRIME>
-__global__ void __launch_bounds__(NT, 3) k_delta(const __grid_constant__ SweepArgs A,
-                                                 const __grid_constant__ CUtensorMap tmv) {
+template <bool PRIME, int TYV = kTYSplit>
+__global__ void __launch_bounds__(Tile<TYV>::NT, 768 / Tile<TYV>::NT)
+    k_delta(const __grid_constant__ SweepArgs A, const __grid_constant__ CUtensorMap tmv) {
+  TEM_TILE_CONSTANTS(TYV);
   extern __shared__ unsigned char smem_raw[];
   double2* ring = smem_align128(smem_raw);   // [R_D][3] tiles
   __shared__ __align__(8) uint64_t bar[R_D];
@@ -777,7 +800,7 @@ __global__ void __launch_bounds__(NT, 3) k_delta(const __grid_constant__ SweepAr
   const Grid& g = A.g;
   int a, tx0, ty0, kb, ke;
   int pidx;
-  block_coords(A, a, tx0, ty0, kb, ke, pidx);
+  block_coords<TYV>(A, a, tx0, ty0, kb, ke, pidx);
   const int tid = threadIdx.x;
   bool live = a < A.ctl->n_active;
   int s = 0;
@@ -789,7 +812,7 @@ __global__ void __launch_bounds__(NT, 3) k_delta(const __grid_constant__ SweepAr
   }
   double2 acc = czero();
   if (live) {
-    const Column C = make_column(g, tx0, ty0);
+    const Column C = make_column<TYV>(g, tx0, ty0);
     for (int q = tid; q < ke - kb; q += NT) {
       zih[q] = __ldg(g.ih[2] + kb + q);
       zhd[q] = __ldg(g.hdm[2] + kb + q);
@@ -829,7 +852,7 @@ __global__ void __launch_bounds__(NT, 3) k_delta(const __grid_constant__ SweepAr
       const double2* S0 = ring + (k % R_D) * 3 * TS2;
       const double2* S1 = ring + ((k + 1) % R_D) * 3 * TS2;
       double2 v[3];
-      const double2 fq = faces_quad(C, zih[k - kb], zhd[k - kb], S0, S1, S0 + TS2, S1 + TS2, S0 + 2 * TS2, v);
+      const double2 fq = faces_quad<TYV>(C, zih[k - kb], zhd[k - kb], S0, S1, S0 + TS2, S1 + TS2, S0 + 2 * TS2, v);
       double2 mq = cscale(mN[0], csq(v[0]));
       mq = cfma(make_double2(mN[1], 0.0), csq(v[1]), mq);
       mq = cfma(make_double2(mN[2], 0.0), csq(v[2]), mq);
@@ -849,7 +872,7 @@ __global__ void __launch_bounds__(NT, 3) k_delta(const __grid_constant__ SweepAr
     A.part[8 * A.pstride + pidx] = acc.y;
   }
   if (!last_block(&A.ctl->ticket[PRIME ? 6 : 5])) return;
-  finalize_split<PRIME>(A);
+  finalize_split<PRIME, TYV>(A);
 }
 
 }  // namespace tem
