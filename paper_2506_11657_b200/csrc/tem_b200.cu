@@ -316,7 +316,7 @@ static int sweep_attrs() {
   TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<0>, (cudaFuncAttribute)attr, (int)T2::kSmemDirect));
   TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<2>, (cudaFuncAttribute)attr, (int)T2::kSmemDirect));
   TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<1>, (cudaFuncAttribute)attr, (int)T2::kSmemDirap));
-  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<3>, (cudaFuncAttribute)attr, (int)TS::kSmemDirap));
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<3>, (cudaFuncAttribute)attr, (int)TS::kSmemUpd));
   TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<4>, (cudaFuncAttribute)attr, (int)TS::kSmemDirap));
   TEM_CUDA(cudaFuncSetAttribute(tem::k_delta<false>, (cudaFuncAttribute)attr, (int)TS::kSmemDelta));
   TEM_CUDA(cudaFuncSetAttribute(tem::k_delta<true>, (cudaFuncAttribute)attr, (int)TS::kSmemDelta));
@@ -424,7 +424,7 @@ int tem_create(int nx, int ny, int nz, const double* hx, const double* hy, const
     using TS = tem::Tile<tem::kTYSplit>;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tem::k_sweep<1>, T2::NT, T2::kSmemDirap);
     c->per_sm_two = std::max(1, per_sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tem::k_sweep<3>, TS::NT, TS::kSmemDirap);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tem::k_sweep<3>, TS::NT, TS::kSmemUpd);
     c->per_sm_split = std::max(1, per_sm);
   }
   *out = c;
@@ -607,7 +607,7 @@ static int solve(tem_ctx* c, const double* mass, const double* f, int S, const d
   auto launch_iter = [&](const Cfg& k, int q, cudaStream_t st_) {
     if (split) {
       if (q == 0)
-        tem::k_sweep<3><<<k.grid, TS::NT, TS::kSmemDirap, st_>>>(k.a1[0], tmP[0], tmZ[0]);
+        tem::k_sweep<3><<<k.grid, TS::NT, TS::kSmemUpd, st_>>>(k.a1[0], tmP[0], tmZ[0]);
       else
         tem::k_sweep<4><<<k.grid, TS::NT, TS::kSmemDirap, st_>>>(k.a1[1], tmP[1], tmZ[1]);
       tem::k_delta<false><<<k.grid, TS::NT, TS::kSmemDelta, st_>>>(k.a2[q], tmZ[1 - q]);

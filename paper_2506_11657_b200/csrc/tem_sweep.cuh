@@ -47,7 +47,8 @@ struct Tile {
   static constexpr int TILE_STRIDE = (TILE_BYTES + 127) / 128 * 128;   // slot pitch (128 B aligned)
   static constexpr int TS2 = TILE_STRIDE / 16;     // slot pitch in double2
   static constexpr size_t kSmemDirect = 128 + (size_t)(2 * R_XY + R_Z) * TILE_STRIDE;
-  static constexpr size_t kSmemDirap = kSmemDirect + (size_t)6 * TILE_STRIDE;
+  static constexpr size_t kSmemDirap = kSmemDirect + (size_t)6 * TILE_STRIDE;    // + z staging, 2 sets
+  static constexpr size_t kSmemUpd = kSmemDirect + (size_t)12 * TILE_STRIDE;     // + z staging, 4 sets
   static constexpr size_t kSmemDelta = 128 + (size_t)3 * R_D * TILE_STRIDE;
 };
 constexpr int kTYTwoSweep = 8;    // tile height of MODE 0, 1, 2
@@ -90,7 +91,7 @@ struct SweepArgs {
   double2* out;                // MODE 0: y; MODE 1, 3, 4: p_new
   double2* x;                  // MODE 2, 4
   double2* z;                  // MODE 2 (in/out); MODE 3, 4: z_{i+1} (out)
-  const double2* zin;          // MODE 3, 4: z_i (own values; the halo comes by TMA)
+  const double2* zin;          // MODE 4: z_i own values (MODE 3 reads them from its TMA staging)
   const double2* pold;         // MODE 4: p_{i-1} (own values)
   ShiftState* st;              // [S]
   Control* ctl;
@@ -551,7 +552,11 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
   double2* rX = ring;                        // [R_XY] slots
   double2* rY = ring + R_XY * TS2;           // [R_XY]
   double2* rZ = ring + 2 * R_XY * TS2;       // [R_Z]
-  double2* zs = ring + (2 * R_XY + R_Z) * TS2;   // MODE 1 z staging [2][3 tiles]
+  // z staging [RS][3 tiles]: 2 sets (MODE 1, 4); 4 sets (MODE 3), so that the
+  // node's own z_i (X, Y of set k-1, Z of set k) is still staged at step k
+  constexpr bool kZOwn = (MODE == 3);   // own z_i from staging (MODE 4: re-read, fewer registers)
+  constexpr int RS = kZOwn ? 4 : 2;
+  double2* zs = ring + (2 * R_XY + R_Z) * TS2;
   __shared__ __align__(8) uint64_t bar[R_XY];
   __shared__ double red[3 * NT / 32];
   __shared__ double zih[kMaxChunk + 1];     // ih_z[k] for k = kb-1 .. ke-1
@@ -615,7 +620,7 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
       tma_tile(rY + sx * TS2, &tmv, cx, cy, q + 1, 1, s, &bar[sx]);
       if (with_z) tma_tile(rZ + sz * TS2, &tmv, cx, cy, q, 2, s, &bar[sx]);
       if (kZ) {
-        double2* d = zs + pmod(q, 2) * 3 * TS2;
+        double2* d = zs + pmod(q, RS) * 3 * TS2;
         tma_tile(d, &tmz, cx, cy, q + 1, 0, s, &bar[sx]);
         tma_tile(d + TS2, &tmz, cx, cy, q + 1, 1, s, &bar[sx]);
         if (with_z) tma_tile(d + 2 * TS2, &tmz, cx, cy, q, 2, s, &bar[sx]);
@@ -630,7 +635,7 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
     // MODE 1: wait for set q and form p_new = z + beta p_old in its ring slots
     auto combine = [&](int q) {
       wait_set(q);
-      const double2* d = zs + pmod(q, 2) * 3 * TS2;
+      const double2* d = zs + pmod(q, RS) * 3 * TS2;
       double2* dX = rX + pmod(q, R_XY) * TS2;
       double2* dY = rY + pmod(q, R_XY) * TS2;
       double2* dZ = rZ + pmod(q, R_Z) * TS2;
@@ -667,7 +672,7 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
       }
     }
 
-    // centre operands (mass; MODE 2: x, z) of the next step, loaded a step ahead
+    // centre operands (mass; MODE 2: x, z; MODE 4: x, z) of the next step, loaded a step ahead
     auto node_of = [&](int k) { return ((long long)k * ny1 + C.j) * nx1 + C.i; };
     double mN[3];
     double2 xN[3], zN[3];
@@ -682,8 +687,10 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
           xN[c] = ok ? A.x[vs + slot] : czero();
           zN[c] = ok ? A.z[vs + slot] : czero();
         }
-        if (kUpd) zN[c] = ok ? __ldcg(A.zin + vs + slot) : czero();
-        if (MODE == 4) xN[c] = ok ? A.x[vs + slot] : czero();
+        if (MODE == 4) {
+          xN[c] = ok ? A.x[vs + slot] : czero();
+          zN[c] = ok ? __ldcg(A.zin + vs + slot) : czero();
+        }
       }
     };
     load_centre(kb);
@@ -707,6 +714,13 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
       szm = sz0;
       sz0 = sz0 + 1 == R_Z ? 0 : sz0 + 1;
       const long long ek = col + (long long)k * plane;
+      if (kZOwn) {   // own z_i from the staging tiles: X, Y of set k-1, Z of set k
+        const double2* zk1 = zs + pmod(k - 1, RS) * 3 * TS2;
+        const double2* zk = zs + pmod(k, RS) * 3 * TS2;
+        zN[0] = zk1[C.c0];
+        zN[1] = zk1[TS2 + C.c0];
+        zN[2] = zk[2 * TS2 + C.c0];
+      }
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         if (!E.f[c]) continue;
