@@ -99,8 +99,9 @@ __device__ __forceinline__ double kdiag(const Grid& g, int a, const int pos[3]) 
   return tem::edge_weights<2>(g, pos).diag();
 }
 
-// COCG init (z-form): x = 0, p0 = p1 = 0, z = D^-1 f; rho = f^T z, ||f||^2.
-// Block b serves shift b % S.
+// COCG init (z-form): x = 0, p0 = p1 = 0, z = D^-1 f; rho = f^T z, ||f||^2,
+// and (split scheme) the mass part s z^T M z of delta_0.  Block b serves
+// shift b % S; its third partial sum uses A.part[9] / A.part[10] as scratch.
 __global__ void __launch_bounds__(256) k_init(tem::SweepArgs A, double2* p0, double2* p1, double2* z1,
                                               const double* __restrict__ f) {
   __shared__ double red[3 * 8];
@@ -111,7 +112,7 @@ __global__ void __launch_bounds__(256) k_init(tem::SweepArgs A, double2* p0, dou
   const int b = blockIdx.x / S;
   const double2 sh = A.st[s].s;
   const long long vs = (long long)s * 3 * g.Nn;
-  double2 rho = tem::czero();
+  double2 rho = tem::czero(), zmz = tem::czero();
   double rr = 0.0;
   for (long long slot = b * 256LL + threadIdx.x; slot < 3 * g.Nn; slot += (long long)nb * 256) {
     const double m = __ldg(A.mass + slot);
@@ -125,6 +126,7 @@ __global__ void __launch_bounds__(256) k_init(tem::SweepArgs A, double2* p0, dou
       zv = tem::cdiv(make_double2(fv, 0.0), D);
       rho = tem::cfma(make_double2(fv, 0.0), zv, rho);
       rr += fv * fv;
+      zmz = tem::cadd(zmz, tem::cscale(m, tem::csq(zv)));
     }
     A.x[vs + slot] = tem::czero();
     A.z[vs + slot] = zv;
@@ -133,26 +135,35 @@ __global__ void __launch_bounds__(256) k_init(tem::SweepArgs A, double2* p0, dou
     if (z1) z1[vs + slot] = tem::czero();
   }
   tem::block_sum_n<256>(rho, rr, red);
+  double dum = 0.0;
+  tem::block_sum_n<256>(zmz, dum, red);
   if (threadIdx.x == 0) {
     A.part_c[blockIdx.x] = rho;
     A.part_r[blockIdx.x] = rr;
+    A.part[9 * A.pstride + blockIdx.x] = zmz.x;
+    A.part[10 * A.pstride + blockIdx.x] = zmz.y;
   }
   if (!tem::last_block(&A.ctl->ticket[0])) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int q = warp; q < S; q += 8) {
-    double cx = 0, cy = 0, cr = 0;
+    double cx = 0, cy = 0, cr = 0, mx = 0, my = 0;
     for (int bb = q + lane * S; bb < (int)gridDim.x; bb += 32 * S) {
       const double2 v = __ldcg(A.part_c + bb);
       cx += v.x;
       cy += v.y;
       cr += __ldcg(A.part_r + bb);
+      mx += __ldcg(A.part + 9 * A.pstride + bb);
+      my += __ldcg(A.part + 10 * A.pstride + bb);
     }
     cx = tem::warp_sum(cx);
     cy = tem::warp_sum(cy);
     cr = tem::warp_sum(cr);
+    mx = tem::warp_sum(mx);
+    my = tem::warp_sum(my);
     if (lane == 0) {
       tem::ShiftState& st = A.st[q];
       st.rho = make_double2(cx, cy);
+      st.dm0 = tem::cmul(st.s, make_double2(mx, my));   // s z_0^T M z_0
       st.fnorm = sqrt(cr);
       st.relres = cr > 0 ? 1.0 : 0.0;
       st.alpha = tem::czero();

@@ -67,6 +67,7 @@ struct ShiftState {
   double2 alpha;
   double2 beta;
   double2 alpha_prev;   // alpha of the previous iteration (split solver: x every other iteration)
+  double2 dm0;          // split solver: s z_0^T M z_0 (mass part of delta_0, from k_init)
   double fnorm;     // ||f||_2
   double relres;    // ||r||_2 / ||f||_2
   int active;
@@ -105,8 +106,9 @@ struct SweepArgs {
 };
 
 // Split solver (MODE 3/4 pass 1, k_delta pass 2) per-CTA partials:
-// gamma, eps, mu (re, im), ||r||^2 from pass 1; delta (re, im) from pass 2.
-constexpr int kSplitPart = 9;
+// [0..6] pass 1: gamma, eps, mu (re, im), ||r||^2; [7, 8] pass 2: z^T K z;
+// [9, 10] pass 1: s sum_e m_e z_e^2 (the mass part of delta, pointwise)
+constexpr int kSplitPart = 11;
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -344,24 +346,22 @@ __device__ __forceinline__ double2 csq(double2 a) { return make_double2(fma(a.x,
 template <int TYV>
 __device__ __forceinline__ double2 faces_quad(const Column& C, double ihz, double hdz, const double2* X0,
                                               const double2* Xp, const double2* Y0, const double2* Yp,
-                                              const double2* Z0, double2 v[3]) {
+                                              const double2* Z0) {
   constexpr int HX = Tile<TYV>::HX;
   const int c0 = C.c0;
   const double2 x00 = X0[c0], y00 = Y0[c0], z00 = Z0[c0];
   const double2 Fz = csub(cadd(x00, Y0[c0 + 1]), cadd(X0[c0 + HX], y00));
   const double2 Fy = csub(cadd(z00, Xp[c0]), cadd(Z0[c0 + 1], x00));
   const double2 Fx = csub(cadd(y00, Z0[c0 + HX]), cadd(Yp[c0], z00));
-  v[0] = x00;
-  v[1] = y00;
-  v[2] = z00;
   double2 acc = cscale(hdz * C.pxy, csq(Fz));
   acc = cadd(acc, cscale(C.cyx * ihz, csq(Fy)));
   return cadd(acc, cscale(C.cxy * ihz, csq(Fx)));
 }
 
 // ---------------------------------------------------------------- pass 2
-// k_delta: delta = z^T A z of the split solver, per shift, from the node's own
-// faces (faces_quad) and the mass term.  It reads z once (16 B per unknown per
+// k_delta: z^T K z of the split solver, per shift, from the node's own faces
+// (faces_quad); the mass term s z^T M z is pointwise and comes with pass 1
+// (k_init for z_0).  It reads z once (16 B per unknown per
 // shift) with a +1 halo; plane sets q = {X(q), Y(q), Z(q)} in a 4-deep ring
 // (step k reads sets k and k+1, sets k+2 and k+3 in flight): 12 tiles, 66 KB,
 // three CTAs per SM.
@@ -385,19 +385,21 @@ __device__ void finalize_split(const SweepArgs& A) {
 #pragma unroll
     for (int t = 0; t < kSplitPart; ++t) {
       double acc = 0.0;
-      if (!PRIME || t >= 7)
+      if (!PRIME || t == 7 || t == 8)   // PRIME: the mass part of delta_0 is sq.dm0
         for (int b = a * per + lane; b < (a + 1) * per; b += 32) acc += __ldcg(A.part + t * A.pstride + b);
       v[t] = warp_sum(acc);
     }
     if (lane != 0) continue;
     const double2 gam = make_double2(v[0], v[1]), eps = make_double2(v[2], v[3]);
-    const double2 mu = make_double2(v[4], v[5]), del = make_double2(v[7], v[8]);
+    const double2 mu = make_double2(v[4], v[5]);
+    const double2 del = make_double2(v[7] + v[9], v[8] + v[10]);   // z^T K z + s z^T M z
     if (PRIME) {
-      if (del.x == 0.0 && del.y == 0.0) {
+      const double2 del0 = make_double2(v[7] + sq.dm0.x, v[8] + sq.dm0.y);
+      if (del0.x == 0.0 && del0.y == 0.0) {
         sq.active = 0;
         sq.status = 2;
       } else {
-        sq.alpha = cdiv(sq.rho, del);
+        sq.alpha = cdiv(sq.rho, del0);
         sq.alpha_prev = czero();
         sq.beta = czero();
       }
@@ -586,7 +588,7 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
       live = st.active != 0;
     }
   }
-  double2 acc_c = czero(), acc_e = czero(), acc_m = czero();
+  double2 acc_c = czero(), acc_e = czero(), acc_m = czero(), acc_q = czero();
   double acc_r = 0.0;
   // MODE 4: x_{i+1} = x_{i-1} + (alpha_i + a/beta_i) p_i - (a/beta_i) z_i, a = alpha_{i-1}
   // (exact rewrite of alpha_{i-1} p_{i-1} + alpha_i p_i); when |beta_i| < 1/8 the
@@ -742,6 +744,7 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
           acc_r += rn.x * rn.x + rn.y * rn.y;
           acc_e = cfma(zn, q, acc_e);                                     // z_{i+1}^T A p_i
           acc_m = cfma(E.p[c], q, acc_m);                                 // p_i^T A p_i
+          acc_q = cadd(acc_q, cscale(mN[c], csq(zn)));                    // z_{i+1}^T M z_{i+1}
         } else if (MODE == 0) {
           A.out[e] = q;
         } else if (MODE == 1) {
@@ -771,19 +774,21 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
   if (MODE == 0) return;
   if (kUpd) {
     __shared__ double red9[kSplitPart * NT / 32];
-    double v[kSplitPart] = {acc_c.x, acc_c.y, acc_e.x, acc_e.y, acc_m.x, acc_m.y, acc_r, 0.0, 0.0};
-    constexpr int t0 = 0, t1 = 7;
-    for (int t = t0; t < t1; ++t)
-      for (int o = 16; o > 0; o >>= 1) v[t] += __shfl_down_sync(0xffffffffu, v[t], o);
+    const double2 dm = cmul(sh, acc_q);   // s z^T M z
+    double v[kSplitPart] = {acc_c.x, acc_c.y, acc_e.x, acc_e.y, acc_m.x, acc_m.y, acc_r, 0.0, 0.0, dm.x, dm.y};
+#pragma unroll
+    for (int t = 0; t < kSplitPart; ++t)
+      if (t < 7 || t > 8)
+        for (int o = 16; o > 0; o >>= 1) v[t] += __shfl_down_sync(0xffffffffu, v[t], o);
     const int w = tid >> 5, l = tid & 31;
     __syncthreads();
     if (l == 0)
-      for (int t = t0; t < t1; ++t) red9[kSplitPart * w + t] = v[t];
+      for (int t = 0; t < kSplitPart; ++t) red9[kSplitPart * w + t] = v[t];
     __syncthreads();
-    if (tid < t1 - t0) {
+    if (tid < kSplitPart && (tid < 7 || tid > 8)) {
       double acc = 0.0;
-      for (int q = 0; q < NT / 32; ++q) acc += red9[kSplitPart * q + t0 + tid];
-      A.part[(t0 + tid) * A.pstride + pidx] = acc;
+      for (int q = 0; q < NT / 32; ++q) acc += red9[kSplitPart * q + tid];
+      A.part[tid * A.pstride + pidx] = acc;
     }
     return;
   }
@@ -852,26 +857,12 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, 768 / Tile<TYV>::NT)
     if (tid == 0)
       for (int q = kb; q <= min(kb + 3, ke); ++q) issue(q);
     wait_set(kb);
-    const long long plane = (long long)(g.n[0] + 1) * (g.n[1] + 1);
-    const double* mcol = A.mass + (C.in_ij ? (long long)C.j * (g.n[0] + 1) + C.i : 0);
-    double mN[3];
-    auto load_mass = [&](int k) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) mN[c] = C.in_ij ? __ldg(mcol + k * plane + c * g.Nn) : 0.0;
-    };
-    load_mass(kb);
 #pragma unroll 1
     for (int k = kb; k < ke; ++k) {
       wait_set(k + 1);
       const double2* S0 = ring + (k % R_D) * 3 * TS2;
       const double2* S1 = ring + ((k + 1) % R_D) * 3 * TS2;
-      double2 v[3];
-      const double2 fq = faces_quad<TYV>(C, zih[k - kb], zhd[k - kb], S0, S1, S0 + TS2, S1 + TS2, S0 + 2 * TS2, v);
-      double2 mq = cscale(mN[0], csq(v[0]));
-      mq = cfma(make_double2(mN[1], 0.0), csq(v[1]), mq);
-      mq = cfma(make_double2(mN[2], 0.0), csq(v[2]), mq);
-      acc = cadd(acc, cfma(sh, mq, fq));
-      if (k + 1 < ke) load_mass(k + 1);
+      acc = cadd(acc, faces_quad<TYV>(C, zih[k - kb], zhd[k - kb], S0, S1, S0 + TS2, S1 + TS2, S0 + 2 * TS2));
       __syncthreads();   // set k no longer read
       if (tid == 0 && k + 4 <= ke) {
         fence_proxy_async();
