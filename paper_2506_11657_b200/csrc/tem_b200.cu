@@ -295,12 +295,31 @@ static void sweep_geometry(const tem_ctx* c, int S, int nslot, tem::SweepArgs& A
   A.ntx = (c->g.n[0] + 32 - 1) / 32;
   A.nty = (c->g.n[1] + ty - 1) / ty;
   const int per_sm = ty == tem::kTYSplit ? c->per_sm_split : c->per_sm_two;
-  const int target = 4 * c->num_sms * per_sm;
   const int base = A.ntx * A.nty * nslot;
-  int nzc = 1;
-  while (base * nzc < target && c->g.n[2] / (nzc * 2) >= 16) nzc *= 2;
-  if (const char* env = getenv("TEM_FORCE_NZC")) nzc = std::max(1, atoi(env));  // tests
-  nzc = std::max(nzc, (c->g.n[2] + tem::kMaxChunk - 1) / tem::kMaxChunk);
+  // z-chunk count.  W = CTAs / resident CTAs.  Keep >= 4 waves when the grid
+  // allows (a few slow shifts must still fill the machine), and among those
+  // maximise (wave quantisation W / ceil(W): a partial last wave idles SMs) x
+  // (march efficiency kch / (kch + 3): a CTA fills its plane pipeline, ~3
+  // steps, before it computes).  Large config, 14 shifts: 1344 columns = 9.08
+  // waves of 148 -> 2 chunks of 64 planes, 18.2 waves.
+  const int nz = c->g.n[2];
+  const int nzc_min = (nz + tem::kMaxChunk - 1) / tem::kMaxChunk;
+  int nzc = nzc_min;
+  double best = -1.0;
+  bool best_full = false;
+  for (int cand = nzc_min; cand <= 32 && (cand == nzc_min || nz / cand >= 8); ++cand) {
+    const int kch = (nz + cand - 1) / cand;
+    const int nz_eff = (nz + kch - 1) / kch;
+    const double W = (double)base * nz_eff / ((double)c->num_sms * per_sm);
+    const bool full = W >= 4.0;
+    const double score = full ? W / std::ceil(W) * (double)kch / (kch + 3.0) : W;
+    if ((full && !best_full) || (full == best_full && score > best + 1e-9)) {
+      best = score;
+      best_full = full;
+      nzc = cand;
+    }
+  }
+  if (const char* env = getenv("TEM_FORCE_NZC")) nzc = std::max(nzc_min, atoi(env));  // tests
   A.kchunk = (c->g.n[2] + nzc - 1) / nzc;
   A.nzc = (c->g.n[2] + A.kchunk - 1) / A.kchunk;
   *grid = A.ntx * A.nty * A.nzc * nslot;
