@@ -18,9 +18,15 @@
 //                 tiles; writes p_new; mu = p_new^T (K + s M) p_new (COCG sweep 1)
 // MODE 2  upd   : v = p; x += alpha p; z -= alpha D^-1 (K + s M) p;
 //                 rho = (D z)^T z, ||D z||^2                        (COCG sweep 2)
+// MODE 3/4 split pass 1 (even / odd iteration): p_i = z_i + beta p_{i-1} as
+//                 in MODE 1, then z_{i+1} = z_i - alpha D^-1 A p_i and (odd)
+//                 x_{i+1} = x_{i-1} + alpha_{i-1} p_{i-1} + alpha_i p_i;
+//                 partials gamma, eps, mu, ||r||^2, s z^T M z (R10, R11)
+// k_delta         split pass 2: z^T K z by faces; finalises the split scalars
 // z = D^-1 r is stored instead of r (reading "z-form"): r = D z
-// is recovered where needed, so a COCG iteration streams x, z, p_old, p_new
-// at the 128 B / unknown / shift minimum of a two-reduction COCG.
+// is recovered where needed, so the two-sweep iteration streams x, z, p_old,
+// p_new at the 128 B / unknown / shift minimum of a two-reduction COCG, and
+// the split iteration 96 B.
 #pragma once
 #include <cuda.h>
 
@@ -541,7 +547,7 @@ __device__ __forceinline__ void block_coords(const SweepArgs& A, int& a, int& tx
 // arithmetic.  MODE 1: v = p_old is loaded into the ring and z into a 2-slot
 // staging area; when set q has landed it is combined IN PLACE into
 // p_new = z + beta p_old (at the end of step q-1, two sets ahead), so MODE 1
-// needs 20 tiles (110 KB) and also runs 2 CTAs per SM.
+// needs 20 tiles (110 KB at TY = 8) and also runs 2 CTAs per SM.
 template <int MODE, int TYV = (MODE >= 3 ? kTYSplit : kTYTwoSweep)>
 __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
     k_sweep(const __grid_constant__ SweepArgs A, const __grid_constant__ CUtensorMap tmv,
