@@ -47,13 +47,17 @@ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
 __device__ __forceinline__ double2 czero() { return make_double2(0.0, 0.0); }
 // 1/b: hardware reciprocal seed + two Newton steps on |b|^2 (no slow-path
 // branch of the IEEE division; relative error ~1 ulp for normal |b|^2)
-__device__ __forceinline__ double2 crcp(double2 b) {
-  const double n = fma(b.x, b.x, b.y * b.y);
+__device__ __forceinline__ double2 crcp(double2 b, double& n) {
+  n = fma(b.x, b.x, b.y * b.y);
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(n));
   r = fma(r, fma(-n, r, 1.0), r);
   r = fma(r, fma(-n, r, 1.0), r);
   return make_double2(b.x * r, -b.y * r);
+}
+__device__ __forceinline__ double2 crcp(double2 b) {
+  double n;
+  return crcp(b, n);
 }
 
 // Face weights of the four faces around edge (A, pos): W_d(m), W_d(m-e_b), W_b(m), W_b(m-e_d).

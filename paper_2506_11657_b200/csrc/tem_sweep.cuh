@@ -736,7 +736,8 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
         const double2 q = cfma(sh, cscale(mN[c], E.p[c]), E.q[c]);   // (K + s M) v
         if (kUpd) {
           const double2 D = make_double2(E.kd[c] + mN[c] * sh.x, mN[c] * sh.y);
-          const double2 zn = csub(zN[c], cmul(alpha, cmul(q, crcp(D))));   // z_i - alpha D^-1 A p_i
+          double nD;                                                      // |D|^2
+          const double2 zn = csub(zN[c], cmul(alpha, cmul(q, crcp(D, nD))));   // z_i - alpha D^-1 A p_i
           st_stream(A.out + e, E.p[c]);                                   // p_i
           st_stream(A.z + e, zn);                                         // z_{i+1}
           if (MODE == 4) {   // x_{i+1} = x_{i-1} + alpha_{i-1} p_{i-1} + alpha_i p_i
@@ -745,12 +746,12 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
             else   // p_{i-1} = (p_i - z_i) / beta_i: no re-read of p_{i-1}
               st_stream(A.x + e, cfma(xc_z, zN[c], cfma(xc_p, E.p[c], xN[c])));
           }
-          const double2 rn = cmul(D, zn);                                 // r_{i+1} = D z_{i+1}
-          acc_c = cfma(rn, zn, acc_c);                                    // gamma_{i+1}
-          acc_r += rn.x * rn.x + rn.y * rn.y;
+          const double2 zq = csq(zn);                                     // z_{i+1}^2
+          acc_c = cfma(D, zq, acc_c);                  // gamma_{i+1} = (D z)^T z
+          acc_r = fma(nD, fma(zn.x, zn.x, zn.y * zn.y), acc_r);            // ||D z||^2
+          acc_q = make_double2(fma(mN[c], zq.x, acc_q.x), fma(mN[c], zq.y, acc_q.y));   // z^T M z
           acc_e = cfma(zn, q, acc_e);                                     // z_{i+1}^T A p_i
           acc_m = cfma(E.p[c], q, acc_m);                                 // p_i^T A p_i
-          acc_q = cadd(acc_q, cscale(mN[c], csq(zn)));                    // z_{i+1}^T M z_{i+1}
         } else if (MODE == 0) {
           A.out[e] = q;
         } else if (MODE == 1) {
