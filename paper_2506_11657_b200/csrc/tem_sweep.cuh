@@ -597,10 +597,12 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
   double2 acc_c = czero(), acc_e = czero(), acc_m = czero(), acc_q = czero();
   double acc_r = 0.0;
   // MODE 4: x_{i+1} = x_{i-1} + (alpha_i + a/beta_i) p_i - (a/beta_i) z_i, a = alpha_{i-1}
-  // (exact rewrite of alpha_{i-1} p_{i-1} + alpha_i p_i); when |beta_i| < 1/8 the
-  // subtraction p_i - z_i loses digits and p_{i-1} is re-read instead (x_direct).
-  const bool x_direct = MODE == 4 && (A.force_xdirect || beta.x * beta.x + beta.y * beta.y < 1.0 / 64.0);
-  double2 xc_p = czero(), xc_z = czero();
+  // (exact rewrite of alpha_{i-1} p_{i-1} + alpha_i p_i).  Its rounding error,
+  // relative to the x increment, grows like |z_i| / |beta_i p_{i-1}|; when
+  // |beta_i| < 1/32 (about 2% of iterations) p_{i-1} is re-read instead (x_direct).
+  const bool x_direct = MODE == 4 && (A.force_xdirect || beta.x * beta.x + beta.y * beta.y < 1.0 / 1024.0);
+  // x_{i+1} = x_{i-1} + xc_p p_i + xc_z (z_i, or p_{i-1} when x_direct)
+  double2 xc_p = alpha, xc_z = alpha_prev;
   if (MODE == 4 && !x_direct) {
     xc_z = cdiv(alpha_prev, beta);
     xc_p = cadd(alpha, xc_z);
@@ -742,7 +744,7 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
           st_stream(A.z + e, zn);                                         // z_{i+1}
           if (MODE == 4) {   // x_{i+1} = x_{i-1} + alpha_{i-1} p_{i-1} + alpha_i p_i
             if (x_direct)
-              st_stream(A.x + e, cfma(alpha, E.p[c], cfma(alpha_prev, __ldcg(A.pold + e), xN[c])));
+              st_stream(A.x + e, cfma(xc_p, E.p[c], cfma(xc_z, __ldcg(A.pold + e), xN[c])));
             else   // p_{i-1} = (p_i - z_i) / beta_i: no re-read of p_{i-1}
               st_stream(A.x + e, cfma(xc_z, zN[c], cfma(xc_p, E.p[c], xN[c])));
           }
