@@ -294,3 +294,28 @@ def test_split_and_two_sweep_agree():
         rele.append(np.linalg.norm((a - b)[earth]) / np.linalg.norm(b[earth]))
     print(f"split vs two_sweep: M-norm max {max(relM):.2e}, conducting edges max {max(rele):.2e}")
     assert max(relM) <= 1e-6 and max(rele) <= 1e-9, (relM, rele)   # measured 1.5e-8, 4.4e-11
+
+
+def test_shift_partitioned_forward_sums_to_full(monkeypatch):
+    """--partition shifts on one GPU: the per-rank partial forwards
+    (paper_2506_11657_b200.distributed.forward_partial) over a 3-way shift
+    partition add up to the full forward (the NCCL reduce is a plain sum).
+    The z-chunking is pinned so every shift sees the same CTA geometry, and
+    so the same iterates, in the full and in the partial batches."""
+    from paper_2506_11657_b200.distributed import forward_partial, shard_shifts
+    monkeypatch.setenv("TEM_FORCE_NZC", "2")
+    wl = make_workload("tiny")
+    fw, asm, slots, table, sigma, f = _setup(wl)
+    u_full, _, it_full, _ = fw.forward(sigma, f, table, tol=1e-12)
+    parts = shard_shifts(table.shifts, 3)
+    u_sum = torch.zeros_like(u_full)
+    its = np.zeros(table.n_shift, dtype=int)
+    for idx in parts:
+        u, it, _ = forward_partial(fw, sigma, f, table, idx, tol=1e-12)
+        u_sum += u
+        its[idx] = it
+    assert np.array_equal(its, it_full)
+    Xo = ofw.shifted_solves(asm, table.shifts)
+    T = np.linalg.norm(_term_scale(Xo, table), axis=0)
+    d = (u_sum - u_full).cpu().numpy()[:, slots].T
+    assert np.all(np.linalg.norm(d, axis=0) <= 1e-13 * T)
