@@ -271,7 +271,8 @@ struct tem_ctx {
   int per_sm_two = 2;               // resident CTAs per SM of k_sweep<1> (two-sweep geometry)
   int per_sm_split = 1;             // resident CTAs per SM of k_sweep<3> (split geometry)
   int solver = TEM_SOLVER_SPLIT;
-  int band = 4;                     // tile rows per band of the sweep block order (block_coords)
+  int band = 4;                     // tile rows per band of the block order (block_coords), 32x8 tiles
+  int band_split = 8;               // the same for the split scheme's 32x12 tiles (measured best)
 };
 
 static int check_S(int S) {
@@ -291,7 +292,7 @@ static void sweep_geometry(const tem_ctx* c, int S, int nslot, tem::SweepArgs& A
   A.g = c->g;
   A.S = S;
   A.nslot = nslot;
-  A.band = c->band;
+  A.band = ty == tem::kTYSplit ? c->band_split : c->band;
   A.ntx = (c->g.n[0] + 32 - 1) / 32;
   A.nty = (c->g.n[1] + ty - 1) / ty;
   const int per_sm = ty == tem::kTYSplit ? c->per_sm_split : c->per_sm_two;
@@ -447,7 +448,7 @@ int tem_create(int nx, int ny, int nz, const double* hx, const double* hy, const
     tem_destroy(c);
     return rc;
   }
-  if (const char* env = getenv("TEM_BAND")) c->band = atoi(env);   // experiments
+  if (const char* env = getenv("TEM_BAND")) c->band = c->band_split = atoi(env);   // experiments
   {
     int per_sm = 0;
     using T2 = tem::Tile<tem::kTYTwoSweep>;
