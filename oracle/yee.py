@@ -260,3 +260,27 @@ def gradient(grid) -> sp.csr_matrix:
         vals += [np.ones(e.size), -np.ones(e.size)]
     return sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
                          shape=(num.n, (nx + 1) * (ny + 1) * (nz + 1)))
+
+
+def curl_z_observation(grid, U_full, receivers) -> np.ndarray:
+    """ORACLE: -d_t b_z at receivers (§5 P:398-404:
+    -d_t b_z(r_0, t) = e_z . (curl e)(r_0, t) ~ Q^T(r_0) u(t)).
+
+    Reading R12: on the tensor grid the z-component of curl e is
+    constant on each z-normal face and equals the face circulation of the edge
+    line integrals divided by the face area, so Q^T u for a receiver in the
+    face with lower-corner node (i, j, k) is row (i, j, k) of the z-face block
+    of the incidence T, scaled by 1 / (hx_i hy_j).
+
+    U_full: (n_all_edges, K) channel fields in oracle edge order (every edge,
+    boundary edges 0); receivers: iterable of (i, j, k).  Returns (R, K)."""
+    T, _, num = curl_incidence(grid)
+    nx, ny, nz = grid.shape
+    rows = []
+    scale = []
+    for (i, j, k) in receivers:
+        if not (0 <= i < nx and 0 <= j < ny and 0 <= k <= nz):
+            raise ValueError(f"receiver face ({i}, {j}, {k}) outside the grid")
+        rows.append((k * ny + j) * nx + i)        # z-face block comes first in T
+        scale.append(1.0 / (grid.hx[i] * grid.hy[j]))
+    return (T[rows] @ U_full) * np.asarray(scale)[:, None]

@@ -139,3 +139,33 @@ def test_interior_count_matches_grid():
     asm = yee.assemble(wl)
     assert asm.n == wl.grid.n_interior_edges()
     assert asm.numbering.n == wl.grid.n_edges()
+
+
+def test_curl_z_observation_closed_forms():
+    """-d_t b_z = e_z . curl e: a field with constant curl B e_z,
+    e = (-B y / 2, B x / 2, c z) (its edge line integrals are exact for a
+    linear field), observes B at every face; a gradient field observes 0."""
+    from workloads.configs import make_custom
+    wl = make_custom(9, 7, 5, seed=4)
+    g = wl.grid
+    num = yee.EdgeNumbering(*g.shape)
+    xs, ys, zs = [np.concatenate([[0.0], np.cumsum(h)]) for h in (g.hx, g.hy, g.hz)]
+    c, i, j, k = num.keys()
+    B, cz = 2.5, 0.7
+    u = np.empty(num.n)
+    # x-edge (i,j,k): integral of -B y/2 dx along x at y_j = -B y_j/2 hx_i, etc.
+    mx, my, mz = c == 0, c == 1, c == 2
+    u[mx] = -0.5 * B * ys[j[mx]] * g.hx[i[mx]]
+    u[my] = 0.5 * B * xs[i[my]] * g.hy[j[my]]
+    u[mz] = cz * 0.5 * (zs[k[mz] + 1] ** 2 - zs[k[mz]] ** 2)
+    recv = [(0, 0, 0), (8, 6, 5), (3, 2, 2), (5, 6, 1)]
+    got = yee.curl_z_observation(g, u[:, None], recv)
+    np.testing.assert_allclose(got[:, 0], B, rtol=1e-12)
+    # gradient of a random node potential: curl-free, observes 0
+    G = yee.gradient(g)
+    rng = np.random.default_rng(0)
+    phi = rng.normal(size=G.shape[1])
+    got0 = yee.curl_z_observation(g, (G @ phi)[:, None], recv)
+    assert np.abs(got0).max() <= 1e-12 * np.abs(G @ phi).max() / min(g.hx.min(), g.hy.min()) ** 2
+    with pytest.raises(ValueError):
+        yee.curl_z_observation(g, u[:, None], [(9, 0, 0)])
