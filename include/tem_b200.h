@@ -153,6 +153,19 @@ int tem_last_solve_stats(const tem_ctx* ctx, tem_solve_stats* out);
 int tem_synthesize(tem_ctx* ctx, int S, int K, const double* residues, const int* is_pair,
                    const double* x, double* u, void* stream);
 
+/* Receiver observation (§5): -d_t b_z(r_0, t_k) =
+ * e_z . curl e(r_0, t_k) ~ Q^T(r_0) u(t_k).  On the tensor grid (DESIGN.md
+ * reading R12) e_z . curl e is constant on each z-normal face: the
+ * circulation of u around the face divided by its area hx_i hy_j.
+ *   u:          device channel fields double[K][3][Nn] (tem_synthesize)
+ *   receivers:  HOST int[R][3], the lower-corner node (i, j, k) of the face
+ *               holding each receiver (0 <= i < nx, 0 <= j < ny, 0 <= k <= nz;
+ *               receivers on the surface: k = the air-earth node plane)
+ *   out:        device double[K][R]
+ * TEM_EINVAL for a receiver outside the grid.  Synchronises `stream`. */
+int tem_curl_z(tem_ctx* ctx, int K, const double* u, int R, const int* receivers,
+               double* out, void* stream);
+
 /* End-to-end forward with HOST buffers: uploads sigma and f, computes the
  * mass, solves all shifted systems, synthesises all K channels and downloads
  * u (HOST double[K][3][Nn]).  Device memory comes from a workspace cached in

@@ -38,6 +38,7 @@ SIGNATURES = {
     "tem_set_solver": ([_P, ctypes.c_int], ctypes.c_int),
     "tem_get_solver": ([_P], ctypes.c_int),
     "tem_synthesize": ([_P, ctypes.c_int, ctypes.c_int, _D, _I, _P, _P, _P], ctypes.c_int),
+    "tem_curl_z": ([_P, ctypes.c_int, _P, ctypes.c_int, _I, _P, _P], ctypes.c_int),
     "tem_forward_host": ([_P, _D, _D, ctypes.c_int, _D, ctypes.c_int, _D, _I, ctypes.c_double,
                           ctypes.c_int, _D, _I, _D], ctypes.c_int),
     "tem_fit_family": ([ctypes.c_int, _D, _D, ctypes.c_int, ctypes.c_int, _I, _D, _D, _I, _D],

@@ -243,6 +243,23 @@ __global__ void k_synth(Grid g, int S, int K, const double2* __restrict__ res,
   }
 }
 
+// -d_t b_z at receivers (reading R12): the circulation of
+// the channel field u(t_k) around the z-normal face with lower-corner node
+// (i, j, k), divided by the face area.  One thread per (channel, receiver).
+__global__ void k_curl_z(Grid g, int K, int R, const int* __restrict__ rec, const double* __restrict__ u,
+                         double* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= K * R) return;
+  const int kc = t / R, r = t - kc * R;
+  const int i = rec[3 * r], j = rec[3 * r + 1], k = rec[3 * r + 2];
+  const long long nx1 = g.n[0] + 1, ny1 = g.n[1] + 1;
+  const long long node = ((long long)k * ny1 + j) * nx1 + i;
+  const double* uk = u + (long long)kc * 3 * g.Nn;
+  // +x(i,j,k) + y(i+1,j,k) - x(i,j+1,k) - y(i,j,k)
+  const double circ = uk[node] + uk[g.Nn + node + 1] - uk[node + nx1] - uk[g.Nn + node];
+  out[t] = circ * __ldg(g.ih[0] + i) * __ldg(g.ih[1] + j);
+}
+
 }  // namespace
 
 void tem_set_error(const std::string& msg) { g_last_error = msg; }
@@ -817,6 +834,26 @@ int tem_synthesize(tem_ctx* c, int S, int K, const double* residues, const int* 
   TEM_CUDA(cudaGetLastError());
   // synchronise so the pageable host buffers above are not reused early
   TEM_CUDA(cudaStreamSynchronize(stream));
+  return TEM_OK;
+}
+
+int tem_curl_z(tem_ctx* c, int K, const double* u, int R, const int* receivers, double* out, void* stream_) {
+  if (!c || !u || !receivers || !out) return fail(TEM_EINVAL, "tem_curl_z: null pointer");
+  if (K < 1 || R < 1) return fail(TEM_EINVAL, "tem_curl_z: need K >= 1, R >= 1");
+  for (int r = 0; r < R; ++r) {
+    const int i = receivers[3 * r], j = receivers[3 * r + 1], k = receivers[3 * r + 2];
+    if (i < 0 || i >= c->g.n[0] || j < 0 || j >= c->g.n[1] || k < 0 || k > c->g.n[2])
+      return fail(TEM_EINVAL, "tem_curl_z: receiver " + std::to_string(r) + " outside the grid");
+  }
+  const size_t rec_bytes = (size_t)3 * R * sizeof(int);
+  if (int rc = ensure_scratch(c, rec_bytes)) return rc;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  TEM_CUDA(cudaMemcpyAsync(c->scratch, receivers, rec_bytes, cudaMemcpyHostToDevice, stream));
+  const int n = K * R, block = 256;
+  k_curl_z<<<(n + block - 1) / block, block, 0, stream>>>(c->g, K, R, static_cast<const int*>(c->scratch),
+                                                          u, out);
+  TEM_CUDA(cudaGetLastError());
+  TEM_CUDA(cudaStreamSynchronize(stream));   // the host receiver list may be reused on return
   return TEM_OK;
 }
 

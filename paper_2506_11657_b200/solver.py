@@ -246,6 +246,20 @@ class TemForward:
                                            ctypes.c_void_p(u.data_ptr()), _stream_ptr(stream)))
         return u
 
+    def dbzdt(self, u: torch.Tensor, receivers, stream=None) -> torch.Tensor:
+        """-d_t b_z(r_0, t_k) = e_z . curl e at receivers
+        given as z-face lower-corner nodes (i, j, k); u (K, n_slots) from
+        synthesize.  Returns (K, R) on the device."""
+        _need_cuda(u, torch.float64, "u")
+        if u.dim() != 2 or u.shape[1] != self.n_slots:
+            raise ValueError("u must be (K, n_slots)")
+        rec = np.ascontiguousarray(np.asarray(receivers, dtype=np.int32).reshape(-1, 3))
+        K, R = u.shape[0], rec.shape[0]
+        out = torch.empty((K, R), dtype=torch.float64, device=self.device)
+        _lib.check(self.lib.tem_curl_z(self._h, K, ctypes.c_void_p(u.data_ptr()), R, _iptr(rec),
+                                       ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+        return out
+
     def forward_host(self, sigma: np.ndarray, f: np.ndarray, table: RationalTable,
                      tol: float = 1e-10, maxit: int = 100000, out: np.ndarray | None = None):
         """End-to-end with host buffers (tem_forward_host).  Returns

@@ -319,3 +319,26 @@ def test_shift_partitioned_forward_sums_to_full(monkeypatch):
     T = np.linalg.norm(_term_scale(Xo, table), axis=0)
     d = (u_sum - u_full).cpu().numpy()[:, slots].T
     assert np.all(np.linalg.norm(d, axis=0) <= 1e-13 * T)
+
+
+def test_curl_z_observation_vs_oracle():
+    """tem_curl_z (-d_t b_z at receivers, reading R12)
+    against the oracle's observation operator on the channel fields of a
+    forward; receivers at the loop centre, inside and outside the loop, on
+    the surface and below it."""
+    wl = make_workload("tiny")
+    fw, asm, slots, table, sigma, f = _setup(wl)
+    u, _, _, _ = fw.forward(sigma, f, table, tol=1e-12)
+    nx, ny, nz = wl.grid.shape
+    ks = wl.surface_k
+    recv = [(nx // 2, ny // 2, ks), (nx // 2 - 1, ny // 2 - 1, ks), (0, 0, ks), (nx - 1, 2, ks),
+            (nx // 2, ny // 2, ks - 2), (3, 5, nz)]
+    got = fw.dbzdt(u, recv).cpu().numpy()                      # (K, R)
+    c, i, j, k = asm.numbering.keys()
+    U_full = u.cpu().numpy()[:, fw.slot(c, i, j, k)].T       # every edge, oracle order
+    ref = yee.curl_z_observation(wl.grid, U_full, recv).T    # (K, R)
+    scale = np.abs(U_full).max() / (wl.grid.hx.min() * wl.grid.hy.min())
+    assert np.all(np.abs(got - ref) <= 1e-13 * scale)
+    assert np.all(np.abs(ref[:, 0]) > 0)                       # the loop centre sees a transient
+    with pytest.raises(_lib.TemError):
+        fw.dbzdt(u, [(nx, 0, 0)])
