@@ -142,14 +142,29 @@ typedef struct {
   long long shift_iterations; /* sum over shifts of COCG iterations */
   int iterations;             /* max over shifts */
   int grid, block;            /* launch configuration of the sweep kernels */
+  int real_shifts;            /* shifts solved in real arithmetic (split scheme) */
 } tem_solve_stats;
 int tem_last_solve_stats(const tem_ctx* ctx, tem_solve_stats* out);
+
+/* Batched solve with one right-hand side PER SHIFT and per-shift tolerances
+ * (the correction solves of tem_forward's refinement, reading R13):
+ *   (K + shifts[s] M) x_s = rhs_s,  stop when ||rhs_s - A_s x_s|| / ||rhs_s|| <= tols[s]
+ *   rhs:  device shift block (complex, [S][3][Nn]); non-free slots must hold 0.
+ *         A shift with rhs_s = 0 does no iteration and returns x_s = 0.
+ *   tols: HOST double[S] (> 0).  Other arguments as tem_cocg_solve.
+ * A real shift (imag == 0) whose rhs_s is real runs in real arithmetic. */
+int tem_cocg_solve_rhs(tem_ctx* ctx, const double* mass, const double* rhs, int S,
+                       const double* shifts, const double* tols, int maxit, double* x,
+                       void* work, size_t work_bytes, int* iters, double* relres,
+                       void* stream);
 
 /* Channel synthesis, the tall-skinny product of §3.2 (eq:rmj):
  *   u[k][slot] = sum_s w_s Re( residues[k*S + s] * x[s][slot] ),
  *   w_s = 2 if is_pair[s] else 1,   k = 0..K-1
  * residues: HOST complex[K][S]; is_pair: HOST int[S]; x: device shift block;
- * u: device double[K][3][Nn] (non-free slots written 0). */
+ * u: device double[K][3][Nn] (non-free slots written 0).  Asynchronous: the
+ * host arrays are staged through context-owned pinned memory and may be
+ * reused on return.  Calls on one context must be issued on one stream. */
 int tem_synthesize(tem_ctx* ctx, int S, int K, const double* residues, const int* is_pair,
                    const double* x, double* u, void* stream);
 
@@ -162,17 +177,75 @@ int tem_synthesize(tem_ctx* ctx, int S, int K, const double* residues, const int
  *               holding each receiver (0 <= i < nx, 0 <= j < ny, 0 <= k <= nz;
  *               receivers on the surface: k = the air-earth node plane)
  *   out:        device double[K][R]
- * TEM_EINVAL for a receiver outside the grid.  Synchronises `stream`. */
+ * TEM_EINVAL for a receiver outside the grid.  Asynchronous (as
+ * tem_synthesize). */
 int tem_curl_z(tem_ctx* ctx, int K, const double* u, int R, const int* receivers,
                double* out, void* stream);
 
+/* Residual of the shifted systems in double-double arithmetic, rounded to
+ * fp64 (reading R13): r_s = f - (K + shifts[s] M) x_s on every free
+ * edge, 0 elsewhere.  The face weights are the fp64 products the sweeps use,
+ * so K is the operator tem_cocg_solve iterates with; sums and products are
+ * carried to ~1e-32 relative, so r is accurate even when it is 1e-16 of the
+ * terms that cancel in it.  f: device real edge vector; x, r: device shift
+ * blocks (must not alias); rnorm: HOST double[S] (may be NULL) receives
+ * ||r_s||_2 (then the call synchronises `stream`). */
+int tem_residual(tem_ctx* ctx, const double* mass, const double* f, int S, const double* shifts,
+                 const double* x, double* r, double* rnorm, void* stream);
+
+/* The forward of the north star in one call: all shifted solves, channel
+ * synthesis, and -- with max_refine > 0 -- iterative refinement until the
+ * channels are converged (reading R13):
+ *   x_s <- COCG(f) to tol;  u = synthesis(x);  then per round, for the shifts
+ *   still refined: r_s = f - (K + s M) x_s in double-double arithmetic,
+ *   d_s = COCG(r_s) to refine_tol (relative to ||r_s||), x_s += d_s.
+ * Channel-aware stopping: after a round, the change of channel k due to
+ * shift s is ||w_s Re(alpha_ks d_s)||_M / ||u_k||_M (the M-norm of the
+ * paper's error bound); the error left behind is estimated as that
+ * change times min(1, safety * ||r_s after|| / ||r_s before||).  A shift is
+ * refined again while some channel's estimate exceeds channel_tol / S; the
+ * loop ends when every channel's summed estimate is <= channel_tol (or after
+ * max_refine rounds).  u is re-synthesised from the refined x. */
+typedef struct {
+  double tol;          /* COCG tolerance of the first solve (relative residual), e.g. 1e-10 */
+  int maxit;           /* COCG iterations per solve, at most */
+  int max_refine;      /* refinement rounds at most (0: plain solve + synthesis) */
+  double refine_tol;   /* residual reduction asked of each correction solve, in (0, 1) */
+  double channel_tol;  /* target: estimated relative M-norm error of every channel */
+  double safety;       /* >= 1: error-to-residual amplification allowance of the estimate */
+} tem_forward_opts;
+typedef struct {
+  int refine_rounds;                   /* rounds run */
+  long long shift_iterations;          /* COCG shift-iterations of all solves */
+  long long initial_shift_iterations;  /* of the first solve */
+  double loop_ms;                      /* GPU time of all COCG solves */
+  double channel_bound;                /* max_k of the final estimate (-1: no refinement) */
+  double relres_max;                   /* max_s final relative residual (double-double if refined) */
+} tem_forward_stats;
+/* tol 1e-10, maxit 200000, max_refine 0, refine_tol 1e-6, channel_tol 1e-8, safety 100 */
+void tem_forward_default_opts(tem_forward_opts* opts);
+size_t tem_forward_workspace_bytes(const tem_ctx* ctx, int S, int K);
+/*   mass, f: device (tem_edge_mass; real edge vector); shifts, residues
+ *   ([K][S]), is_pair: HOST as tem_synthesize; x: device shift block out;
+ *   u: device double[K][3][Nn] out; work: >= tem_forward_workspace_bytes.
+ *   iters (HOST, may be NULL): COCG iterations per shift over all solves;
+ *   relres (HOST, may be NULL): final relative residual per shift
+ *   (double-double evaluation when refined); fst (HOST, may be NULL).
+ * Synchronises `stream`.  Same error codes as tem_cocg_solve (ENOCONV if a
+ * solve did not converge; x and u still hold the iterate). */
+int tem_forward(tem_ctx* ctx, const double* mass, const double* f, int S, const double* shifts,
+                int K, const double* residues, const int* is_pair, const tem_forward_opts* opts,
+                double* x, double* u, void* work, size_t work_bytes, int* iters,
+                double* relres, tem_forward_stats* fst, void* stream);
+int tem_last_forward_stats(const tem_ctx* ctx, tem_forward_stats* out);
+
 /* End-to-end forward with HOST buffers: uploads sigma and f, computes the
- * mass, solves all shifted systems, synthesises all K channels and downloads
- * u (HOST double[K][3][Nn]).  Device memory comes from a workspace cached in
- * the context.  Synchronous.  Same error codes as tem_cocg_solve. */
+ * mass, runs tem_forward with `opts` and downloads u (HOST double[K][3][Nn]).
+ * Device memory comes from a workspace cached in the context.  Synchronous.
+ * Same error codes as tem_forward. */
 int tem_forward_host(tem_ctx* ctx, const double* sigma, const double* f, int S,
                      const double* shifts, int K, const double* residues,
-                     const int* is_pair, double tol, int maxit, double* u,
+                     const int* is_pair, const tem_forward_opts* opts, double* u,
                      int* iters, double* relres);
 
 /* Host-side construction of the shared-pole family, computed once before the

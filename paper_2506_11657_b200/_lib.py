@@ -15,7 +15,20 @@ _LIB = None
 class SolveStats(ctypes.Structure):
     _fields_ = [("loop_ms", ctypes.c_double), ("kernel_launches", ctypes.c_longlong),
                 ("shift_iterations", ctypes.c_longlong), ("iterations", ctypes.c_int),
-                ("grid", ctypes.c_int), ("block", ctypes.c_int)]
+                ("grid", ctypes.c_int), ("block", ctypes.c_int), ("real_shifts", ctypes.c_int)]
+
+
+class ForwardOpts(ctypes.Structure):
+    """tem_forward_opts (include/tem_b200.h)."""
+    _fields_ = [("tol", ctypes.c_double), ("maxit", ctypes.c_int), ("max_refine", ctypes.c_int),
+                ("refine_tol", ctypes.c_double), ("channel_tol", ctypes.c_double), ("safety", ctypes.c_double)]
+
+
+class ForwardStats(ctypes.Structure):
+    """tem_forward_stats (include/tem_b200.h)."""
+    _fields_ = [("refine_rounds", ctypes.c_int), ("shift_iterations", ctypes.c_longlong),
+                ("initial_shift_iterations", ctypes.c_longlong), ("loop_ms", ctypes.c_double),
+                ("channel_bound", ctypes.c_double), ("relres_max", ctypes.c_double)]
 
 
 _P = ctypes.c_void_p
@@ -39,8 +52,16 @@ SIGNATURES = {
     "tem_get_solver": ([_P], ctypes.c_int),
     "tem_synthesize": ([_P, ctypes.c_int, ctypes.c_int, _D, _I, _P, _P, _P], ctypes.c_int),
     "tem_curl_z": ([_P, ctypes.c_int, _P, ctypes.c_int, _I, _P, _P], ctypes.c_int),
-    "tem_forward_host": ([_P, _D, _D, ctypes.c_int, _D, ctypes.c_int, _D, _I, ctypes.c_double,
-                          ctypes.c_int, _D, _I, _D], ctypes.c_int),
+    "tem_cocg_solve_rhs": ([_P, _P, _P, ctypes.c_int, _D, _D, ctypes.c_int, _P, _P, ctypes.c_size_t, _I,
+                            _D, _P], ctypes.c_int),
+    "tem_forward_default_opts": ([ctypes.POINTER(ForwardOpts)], None),
+    "tem_forward_workspace_bytes": ([_P, ctypes.c_int, ctypes.c_int], ctypes.c_size_t),
+    "tem_forward": ([_P, _P, _P, ctypes.c_int, _D, ctypes.c_int, _D, _I, ctypes.POINTER(ForwardOpts), _P, _P,
+                     _P, ctypes.c_size_t, _I, _D, ctypes.POINTER(ForwardStats), _P], ctypes.c_int),
+    "tem_residual": ([_P, _P, _P, ctypes.c_int, _D, _P, _P, _D, _P], ctypes.c_int),
+    "tem_last_forward_stats": ([_P, ctypes.POINTER(ForwardStats)], ctypes.c_int),
+    "tem_forward_host": ([_P, _D, _D, ctypes.c_int, _D, ctypes.c_int, _D, _I, ctypes.POINTER(ForwardOpts),
+                          _D, _I, _D], ctypes.c_int),
     "tem_fit_family": ([ctypes.c_int, _D, _D, ctypes.c_int, ctypes.c_int, _I, _D, _D, _I, _D],
                        ctypes.c_int),
 }

@@ -40,8 +40,11 @@
 #include "../../include/tem_b200.h"
 #include "tem_device.cuh"
 #include "tem_sweep.cuh"
+#include "tem_refine.cuh"
 
 using tem::Grid;
+using tem::k_channel_mnorm;
+using tem::k_rows_sum;
 
 namespace {
 
@@ -99,41 +102,70 @@ __device__ __forceinline__ double kdiag(const Grid& g, int a, const int pos[3]) 
   return tem::edge_weights<2>(g, pos).diag();
 }
 
-// COCG init (z-form): x = 0, p0 = p1 = 0, z = D^-1 f; rho = f^T z, ||f||^2,
-// and (split scheme) the mass part s z^T M z of delta_0.  Block b serves
-// shift b % S; its third partial sum uses A.part[9] / A.part[10] as scratch.
+// COCG init (z-form): x = 0, p0 = p1 = 0, z = D^-1 b; rho = b^T z, ||b||^2,
+// and (split scheme) the mass part s z^T M z of delta_0, with b = f (one real
+// right-hand side for every shift) or b = rhs[s] (a shift block).  Block q
+// serves shift q % S; a real shift (ShiftState::real) is laid out as a real
+// vector (tem::vbase).  Its third partial sum uses A.part[9] / A.part[10] as
+// scratch.
+template <typename V>
+__device__ __forceinline__ void init_body(const tem::SweepArgs& A, int s, int b, int nb, double2* p0,
+                                          double2* p1, double2* z1, const double* __restrict__ f, double2& rho2,
+                                          double& rr, double2& zmz2) {
+  const Grid& g = A.g;
+  const double2 sh2 = A.st[s].s;
+  const long long cst = tem::vcomp<V>(g);
+  const int rowp = tem::vrow<V>(g), nx1 = g.n[0] + 1;
+  V* xv = tem::vbase<V>(A.x, s, g);
+  V* zv = tem::vbase<V>(A.z, s, g);
+  V* p0v = tem::vbase<V>(p0, s, g);
+  V* p1v = tem::vbase<V>(p1, s, g);
+  V* z1v = z1 ? tem::vbase<V>(z1, s, g) : nullptr;
+  const double2* rhs = A.rhs ? A.rhs + (long long)s * 3 * g.Nn : nullptr;
+  V rho = tem::VT<V>::zero(), zmz = tem::VT<V>::zero();
+  for (long long slot = b * 256LL + threadIdx.x; slot < 3 * cst; slot += (long long)nb * 256) {
+    const int a = (int)(slot / cst);
+    const long long nv = slot - a * cst;                 // node in this layout
+    const long long row = nv / rowp;
+    const int i = (int)(nv - row * rowp);
+    V zv_ = tem::VT<V>::zero();
+    if (i < nx1) {
+      const long long abi = a * g.Nn + row * nx1 + i;    // slot in the ABI layout
+      const double m = __ldg(A.mass + abi);
+      if (m > 0.0) {
+        int pos[3];
+        tem::node_pos(g, abi - a * g.Nn, pos);
+        const V D = tem::VT<V>::make(kdiag(g, a, pos) + m * sh2.x, m * sh2.y);
+        const V fv = rhs ? tem::VT<V>::from(__ldg(rhs + abi)) : tem::VT<V>::make(__ldg(f + abi), 0.0);
+        zv_ = tem::cdiv(fv, D);
+        rho = tem::cfma(fv, zv_, rho);
+        rr += tem::cabs2(fv);
+        zmz = tem::sfma(m, tem::csq(zv_), zmz);
+      }
+    }
+    xv[slot] = tem::VT<V>::zero();
+    zv[slot] = zv_;
+    p0v[slot] = tem::VT<V>::zero();
+    p1v[slot] = tem::VT<V>::zero();
+    if (z1v) z1v[slot] = tem::VT<V>::zero();
+  }
+  rho2 = tem::VT<V>::cplx(rho);
+  zmz2 = tem::VT<V>::cplx(zmz);
+}
+
 __global__ void __launch_bounds__(256) k_init(tem::SweepArgs A, double2* p0, double2* p1, double2* z1,
                                               const double* __restrict__ f) {
   __shared__ double red[3 * 8];
-  const Grid& g = A.g;
   const int S = A.S;
   const int s = blockIdx.x % S;
   const int nb = gridDim.x / S;
   const int b = blockIdx.x / S;
-  const double2 sh = A.st[s].s;
-  const long long vs = (long long)s * 3 * g.Nn;
   double2 rho = tem::czero(), zmz = tem::czero();
   double rr = 0.0;
-  for (long long slot = b * 256LL + threadIdx.x; slot < 3 * g.Nn; slot += (long long)nb * 256) {
-    const double m = __ldg(A.mass + slot);
-    double2 zv = tem::czero();
-    if (m > 0.0) {
-      const int a = (int)(slot / g.Nn);
-      int pos[3];
-      tem::node_pos(g, slot - a * g.Nn, pos);
-      const double2 D = make_double2(kdiag(g, a, pos) + m * sh.x, m * sh.y);
-      const double fv = __ldg(f + slot);
-      zv = tem::cdiv(make_double2(fv, 0.0), D);
-      rho = tem::cfma(make_double2(fv, 0.0), zv, rho);
-      rr += fv * fv;
-      zmz = tem::cadd(zmz, tem::cscale(m, tem::csq(zv)));
-    }
-    A.x[vs + slot] = tem::czero();
-    A.z[vs + slot] = zv;
-    p0[vs + slot] = tem::czero();
-    p1[vs + slot] = tem::czero();
-    if (z1) z1[vs + slot] = tem::czero();
-  }
+  if (A.st[s].real)
+    init_body<double>(A, s, b, nb, p0, p1, z1, f, rho, rr, zmz);
+  else
+    init_body<double2>(A, s, b, nb, p0, p1, z1, f, rho, rr, zmz);
   tem::block_sum_n<256>(rho, rr, red);
   double dum = 0.0;
   tem::block_sum_n<256>(zmz, dum, red);
@@ -183,20 +215,68 @@ __global__ void __launch_bounds__(256) k_init(tem::SweepArgs A, double2* p0, dou
   }
 }
 
+// A real shift may run in real arithmetic only if its right-hand side is
+// real: flag[s] = 1 if rhs[s] has a nonzero imaginary part (rhs-block solves).
+__global__ void k_rhs_imag(const double2* __restrict__ rhs, long long nslots, int* flag) {
+  const int s = blockIdx.y;
+  const double2* r = rhs + (long long)s * nslots;
+  bool any = false;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nslots; i += (long long)gridDim.x * blockDim.x)
+    any |= __ldg(&r[i].y) != 0.0;
+  if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(flag + s, 1);
+}
+
 // Split solver epilogue: a shift whose last iteration i was even (iters odd)
 // has x_i in x (x advances every second iteration); x_{i+1} = x_i + alpha_i p_i
 // with p_i in p1.  alpha_i is `alpha` if the shift stopped, `alpha_prev` if it
-// is still running (maxit reached).  Block b serves shift b % S.
+// is still running (maxit reached).  Block q serves shift q % S.
+template <typename V>
+__device__ __forceinline__ void xfix_body(const tem::SweepArgs& A, const double2* p1, int s, int b, int nb,
+                                          double2 a2) {
+  const long long n = 3 * tem::vcomp<V>(A.g);
+  V* x = tem::vbase<V>(A.x, s, A.g);
+  const V* p = tem::vbase<V>(p1, s, A.g);
+  const V a = tem::VT<V>::from(a2);
+  for (long long slot = b * 256LL + threadIdx.x; slot < n; slot += (long long)nb * 256)
+    x[slot] = tem::cfma(a, p[slot], x[slot]);
+}
+
 __global__ void __launch_bounds__(256) k_xfix(tem::SweepArgs A, const double2* __restrict__ p1) {
   const int S = A.S;
   const int s = blockIdx.x % S;
   const tem::ShiftState& st = A.st[s];
   if ((st.iters & 1) == 0) return;
   const double2 a = st.active ? st.alpha_prev : st.alpha;
-  const long long vs = (long long)s * 3 * A.g.Nn;
-  const int nb = gridDim.x / S;
-  for (long long slot = (blockIdx.x / S) * 256LL + threadIdx.x; slot < 3 * A.g.Nn; slot += (long long)nb * 256)
-    A.x[vs + slot] = tem::cfma(a, p1[vs + slot], A.x[vs + slot]);
+  if (st.real)
+    xfix_body<double>(A, p1, s, blockIdx.x / S, gridDim.x / S, a);
+  else
+    xfix_body<double2>(A, p1, s, blockIdx.x / S, gridDim.x / S, a);
+}
+
+// Real shifts: x (real layout, in x's own region) -> complex ABI layout.
+// Pass 0 copies the real vector to tmp (the same shift's region of a free
+// work vector); pass 1 expands tmp into x (imaginary parts 0, non-free and
+// non-existent slots 0).
+__global__ void __launch_bounds__(256) k_real_out(tem::SweepArgs A, double2* tmp, int pass) {
+  const int S = A.S;
+  const int s = blockIdx.x % S;
+  if (!A.st[s].real) return;
+  const int b = blockIdx.x / S, nb = gridDim.x / S;
+  const Grid& g = A.g;
+  const double* xr = tem::vbase<double>(A.x, s, g);
+  double* tr = tem::vbase<double>(tmp, s, g);
+  if (pass == 0) {
+    for (long long i = b * 256LL + threadIdx.x; i < 3 * g.NnP; i += (long long)nb * 256) tr[i] = xr[i];
+    return;
+  }
+  double2* xc = A.x + (long long)s * 3 * g.Nn;
+  const int nx1 = g.n[0] + 1;
+  for (long long slot = b * 256LL + threadIdx.x; slot < 3 * g.Nn; slot += (long long)nb * 256) {
+    const int a = (int)(slot / g.Nn);
+    const long long node = slot - a * g.Nn;
+    const long long row = node / nx1;
+    xc[slot] = make_double2(tr[a * g.NnP + row * g.px + (node - row * nx1)], 0.0);
+  }
 }
 
 // u[k][slot] = sum_s w_s Re(res[k][s] x[s][slot]); 0 on non-free slots.
@@ -273,10 +353,10 @@ struct tem_ctx {
   double* dev_h = nullptr;          // ih[3] and hdm[3] packed
   cudaStream_t cap_stream = nullptr;
   int* pinned_active = nullptr;
-  // cached graphs of kChunk COCG iterations, per (slots, z-chunks), for one set of buffers
-  std::map<long long, cudaGraphExec_t> graphs;
-  std::vector<const void*> graph_key;
-  int graph_S = 0;
+  // cached graphs of kChunk COCG iterations: per set of buffers (+ scheme, S),
+  // per (slots, z-chunks); a few buffer sets (a forward alternates the
+  // initial solve and the correction solves of the refinement)
+  std::map<std::vector<const void*>, std::map<long long, cudaGraphExec_t>> graphs;
   // scratch
   void* scratch = nullptr;          // residues etc.
   size_t scratch_bytes = 0;
@@ -290,6 +370,15 @@ struct tem_ctx {
   int solver = TEM_SOLVER_SPLIT;
   int band = 4;                     // tile rows per band of the block order (block_coords), 32x8 tiles
   int band_split = 8;               // the same for the split scheme's 32x12 tiles (measured best)
+  int real_arith = 1;               // real shifts in real arithmetic (split scheme; TEM_NO_REAL=1 disables)
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;   // loop timing of the last solve
+  double last_fnorm = 0.0;          // ||rhs||_2 of shift 0 of the last solve
+  tem_forward_stats fstats{};       // of the last tem_forward / tem_forward_host
+  void* pin = nullptr;              // pinned staging of small host arrays
+  size_t pin_bytes = 0;
+  cudaEvent_t stage_ev = nullptr;   // last copy out of `pin`
+  void* red = nullptr;              // reduction scratch of tem_residual
+  size_t red_bytes = 0;
 };
 
 static int check_S(int S) {
@@ -299,6 +388,18 @@ static int check_S(int S) {
 }
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Every launching call runs on the device the context was created on; a
+// different current device is an argument error (the caller's streams and
+// buffers would belong to another device).
+static int check_device(const tem_ctx* c) {
+  int dev = -1;
+  TEM_CUDA(cudaGetDevice(&dev));
+  if (dev != c->device)
+    return fail(TEM_EINVAL, "current device " + std::to_string(dev) + " is not the context's device " +
+                                std::to_string(c->device));
+  return TEM_OK;
+}
 
 // sweep geometry of one scheme: xy tiles x z-chunks x shift slots, for tile
 // height ty (tem::kTYTwoSweep or tem::kTYSplit).  The z-range is split until
@@ -355,9 +456,10 @@ static int max_sweep_grid(const tem_ctx* c, int S) {
   return gmax;
 }
 
+// Dynamic shared-memory limits of the sweep kernels.  Function attributes
+// belong to the CUDA context of the current device, so they are set on every
+// tem_create (cheap) rather than once per process.
 static int sweep_attrs() {
-  static bool done = false;
-  if (done) return TEM_OK;
   using T2 = tem::Tile<tem::kTYTwoSweep>;
   using TS = tem::Tile<tem::kTYSplit>;
   const int attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
@@ -368,13 +470,16 @@ static int sweep_attrs() {
   TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<4>, (cudaFuncAttribute)attr, (int)TS::kSmemDirap));
   TEM_CUDA(cudaFuncSetAttribute(tem::k_delta<false>, (cudaFuncAttribute)attr, (int)TS::kSmemDelta));
   TEM_CUDA(cudaFuncSetAttribute(tem::k_delta<true>, (cudaFuncAttribute)attr, (int)TS::kSmemDelta));
-  done = true;
   return TEM_OK;
 }
 
 // 5-D tiled tensor map over a shift block [S][3][nz+1][ny+1][nx+1] complex
 // fp64 (as 2(nx+1) doubles innermost); box = one halo-extended plane tile.
-static int make_tmap(const tem_ctx* c, int S, const void* base, CUtensorMap* tm, int ty = tem::kTYTwoSweep) {
+// real = true: the same buffer in the real layout of real shifts (fp64
+// [3][nz+1][ny+1][px] at the start of each shift's complex region;
+// tem::Grid::px), box 34 x (ty+2) doubles.
+static int make_tmap(const tem_ctx* c, int S, const void* base, CUtensorMap* tm, int ty = tem::kTYTwoSweep,
+                     bool real = false) {
   const int box_x = 32 + 2, box_y = ty + 2;   // halo-extended plane tile (Tile<ty>::HX, HY)
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
@@ -386,9 +491,12 @@ static int make_tmap(const tem_ctx* c, int S, const void* base, CUtensorMap* tm,
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   const cuuint64_t nx1 = c->g.n[0] + 1, ny1 = c->g.n[1] + 1, nz1 = c->g.n[2] + 1;
-  const cuuint64_t dims[5] = {2 * nx1, ny1, nz1, 3, (cuuint64_t)S};
-  const cuuint64_t strides[4] = {16 * nx1, 16 * nx1 * ny1, 16 * nx1 * ny1 * nz1, 48 * nx1 * ny1 * nz1};
-  const cuuint32_t box[5] = {2 * (cuuint32_t)box_x, (cuuint32_t)box_y, 1, 1, 1};
+  const cuuint64_t px = c->g.px, shift_stride = 48 * nx1 * ny1 * nz1;
+  const cuuint64_t dims_c[5] = {2 * nx1, ny1, nz1, 3, (cuuint64_t)S};
+  const cuuint64_t str_c[4] = {16 * nx1, 16 * nx1 * ny1, 16 * nx1 * ny1 * nz1, shift_stride};
+  const cuuint64_t dims_r[5] = {nx1, ny1, nz1, 3, (cuuint64_t)S};
+  const cuuint64_t str_r[4] = {8 * px, 8 * px * ny1, 8 * px * ny1 * nz1, shift_stride};
+  const cuuint32_t box[5] = {(real ? 1u : 2u) * (cuuint32_t)box_x, (cuuint32_t)box_y, 1, 1, 1};
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   if (const char* env = getenv("TEM_L2PROMO")) {  // experiments
@@ -397,8 +505,8 @@ static int make_tmap(const tem_ctx* c, int S, const void* base, CUtensorMap* tm,
           : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
           : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   }
-  CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<void*>(base), dims, strides,
-                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+  CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<void*>(base), real ? dims_r : dims_c,
+                      real ? str_r : str_c, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                       promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(TEM_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return TEM_OK;
@@ -423,13 +531,21 @@ int tem_create(int nx, int ny, int nz, const double* hx, const double* hy, const
     for (int i = 0; i < n[a]; ++i)
       if (!(h[a][i] > 0.0)) return fail(TEM_EINVAL, "tem_create: cell widths must be > 0");
   tem_ctx* c = new tem_ctx();
-  cudaGetDevice(&c->device);
-  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
+  {
+    cudaError_t e0 = cudaGetDevice(&c->device);
+    if (e0 == cudaSuccess) e0 = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
+    if (e0 != cudaSuccess) {
+      delete c;
+      return fail(TEM_ECUDA, std::string("tem_create: ") + cudaGetErrorString(e0));
+    }
+  }
   for (int a = 0; a < 3; ++a) c->g.n[a] = n[a];
   c->g.st[0] = 1;
   c->g.st[1] = nx + 1;
   c->g.st[2] = (long long)(nx + 1) * (ny + 1);
   c->g.Nn = Nn;
+  c->g.px = (nx + 1 + 1) / 2 * 2;
+  c->g.NnP = (long long)c->g.px * (ny + 1) * (nz + 1);
   // host tables: 1/h and hdual/mu0
   std::vector<double> tab;
   size_t off_ih[3], off_hd[3];
@@ -466,14 +582,23 @@ int tem_create(int nx, int ny, int nz, const double* hx, const double* hy, const
     return rc;
   }
   if (const char* env = getenv("TEM_BAND")) c->band = c->band_split = atoi(env);   // experiments
+  if (const char* env = getenv("TEM_NO_REAL")) c->real_arith = atoi(env) ? 0 : 1;  // experiments, tests
   {
     int per_sm = 0;
     using T2 = tem::Tile<tem::kTYTwoSweep>;
     using TS = tem::Tile<tem::kTYSplit>;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tem::k_sweep<1>, T2::NT, T2::kSmemDirap);
+    cudaError_t e1 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tem::k_sweep<1>, T2::NT, T2::kSmemDirap);
     c->per_sm_two = std::max(1, per_sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tem::k_sweep<3>, TS::NT, TS::kSmemUpd);
+    if (e1 == cudaSuccess)
+      e1 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tem::k_sweep<3>, TS::NT, TS::kSmemUpd);
     c->per_sm_split = std::max(1, per_sm);
+    if (e1 == cudaSuccess) e1 = cudaEventCreate(&c->ev0);
+    if (e1 == cudaSuccess) e1 = cudaEventCreate(&c->ev1);
+    if (e1 == cudaSuccess) e1 = cudaEventCreateWithFlags(&c->stage_ev, cudaEventDisableTiming);
+    if (e1 != cudaSuccess) {
+      tem_destroy(c);
+      return fail(TEM_ECUDA, std::string("tem_create: ") + cudaGetErrorString(e1));
+    }
   }
   *out = c;
   return TEM_OK;
@@ -481,11 +606,17 @@ int tem_create(int nx, int ny, int nz, const double* hx, const double* hy, const
 
 void tem_destroy(tem_ctx* c) {
   if (!c) return;
-  for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& set : c->graphs)
+    for (auto& kv : set.second) cudaGraphExecDestroy(kv.second);
   if (c->dev_h) cudaFree(c->dev_h);
   if (c->scratch) cudaFree(c->scratch);
   if (c->e2e) cudaFree(c->e2e);
   if (c->pinned_active) cudaFreeHost(c->pinned_active);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->stage_ev) cudaEventDestroy(c->stage_ev);
+  if (c->red) cudaFree(c->red);
+  if (c->pin) cudaFreeHost(c->pin);
+  if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   delete c;
 }
@@ -500,6 +631,7 @@ size_t tem_num_unknowns(const tem_ctx* c) {
 
 int tem_edge_mass(tem_ctx* c, const double* sigma, double* mass, void* stream) {
   if (!c || !sigma || !mass) return fail(TEM_EINVAL, "tem_edge_mass: null pointer");
+  if (int rc = check_device(c)) return rc;
   const long long total = 3 * c->g.Nn;
   const int block = 256;
   const int grid = (int)std::min<long long>((total + block - 1) / block, (long long)c->num_sms * 32);
@@ -512,6 +644,7 @@ int tem_apply_shifted(tem_ctx* c, const double* mass, int S, const double* shift
                       const double* x, double* y, void* stream) {
   if (!c || !mass || !shifts || !x || !y) return fail(TEM_EINVAL, "tem_apply_shifted: null pointer");
   if (int rc = check_S(S)) return rc;
+  if (int rc = check_device(c)) return rc;
   tem::SweepArgs A{};
   int grid = 0;
   sweep_geometry(c, S, S, A, &grid);
@@ -522,13 +655,13 @@ int tem_apply_shifted(tem_ctx* c, const double* mass, int S, const double* shift
   if (int rc = make_tmap(c, S, x, &tm)) return rc;
   TEM_CUDA(cudaMemsetAsync(y, 0, (size_t)3 * c->g.Nn * S * sizeof(double2), (cudaStream_t)stream));
   using T2 = tem::Tile<tem::kTYTwoSweep>;
-  tem::k_sweep<0><<<grid, T2::NT, T2::kSmemDirect, (cudaStream_t)stream>>>(A, tm, tm);
+  tem::k_sweep<0><<<grid, T2::NT, T2::kSmemDirect, (cudaStream_t)stream>>>(A, tm, tm, tm, tm);
   TEM_CUDA(cudaGetLastError());
   return TEM_OK;
 }
 
 struct WorkLayout {
-  size_t z, z1, p0, p1, st, ctl, part_c, part_r, part9, total;
+  size_t z, z1, p0, p1, st, ctl, flags, part_c, part_r, part9, total;
   size_t nparts;
 };
 
@@ -544,6 +677,7 @@ static WorkLayout work_layout(const tem_ctx* c, int S) {
   L.p1 = o;     o = align_up(o + vec, 256);
   L.st = o;     o = align_up(o + sizeof(tem::ShiftState) * TEM_MAX_SHIFTS, 256);
   L.ctl = o;    o = align_up(o + sizeof(tem::Control), 256);
+  L.flags = o;  o = align_up(o + sizeof(int) * TEM_MAX_SHIFTS, 256);
   L.part_c = o; o = align_up(o + nparts * sizeof(double2), 256);
   L.part_r = o; o = align_up(o + nparts * sizeof(double), 256);
   L.part9 = o;  o = align_up(o + tem::kSplitPart * nparts * sizeof(double), 256);
@@ -572,23 +706,21 @@ size_t tem_cocg_workspace_bytes(const tem_ctx* c, int S) {
 // z-chunking); each is captured once as a CUDA graph of kChunk iterations.
 // The host reads the active count once per graph.
 static int finish_solve(tem_ctx* c, int S, std::vector<tem::ShiftState>& st, const tem::ShiftState* dev_st,
-                        cudaEvent_t ev0, cudaEvent_t ev1, cudaStream_t stream, long long launches, int grid,
-                        int block, int* iters, double* relres) {
+                        cudaStream_t stream, long long launches, int grid, int block, int* iters, double* relres) {
   TEM_CUDA(cudaMemcpyAsync(st.data(), dev_st, sizeof(tem::ShiftState) * S, cudaMemcpyDeviceToHost, stream));
   TEM_CUDA(cudaStreamSynchronize(stream));
   float ms = 0.f;
-  cudaEventElapsedTime(&ms, ev0, ev1);
-  cudaEventDestroy(ev0);
-  cudaEventDestroy(ev1);
+  TEM_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
 
   long long shift_iters = 0;
-  int max_it = 0;
+  int max_it = 0, n_real = 0;
   int status = TEM_OK;
   for (int s = 0; s < S; ++s) {
     if (iters) iters[s] = st[s].iters;
     if (relres) relres[s] = st[s].relres;
     shift_iters += st[s].iters;
     max_it = std::max(max_it, st[s].iters);
+    n_real += st[s].real ? 1 : 0;
     if (st[s].status == 2) status = TEM_EBREAKDOWN;
     else if (st[s].status != 1 && status == TEM_OK) status = TEM_ENOCONV;
   }
@@ -598,14 +730,24 @@ static int finish_solve(tem_ctx* c, int S, std::vector<tem::ShiftState>& st, con
   c->stats.iterations = max_it;
   c->stats.grid = grid;   // with all shifts active
   c->stats.block = block;
+  c->stats.real_shifts = n_real;
+  c->last_fnorm = S > 0 ? st[0].fnorm : 0.0;
   if (status == TEM_EBREAKDOWN) return fail(status, "tem_cocg_solve: COCG breakdown");
   if (status == TEM_ENOCONV) return fail(status, "tem_cocg_solve: not converged within maxit");
   return TEM_OK;
 }
 
-static int solve(tem_ctx* c, const double* mass, const double* f, int S, const double* shifts, double tol,
-                 int maxit, double* x, char* w, const WorkLayout& L, int* iters, double* relres,
-                 cudaStream_t stream) {
+// clears ShiftState::real of shifts whose right-hand side is complex
+__global__ void k_real_mask(tem::ShiftState* st, const int* flag, int S) {
+  const int s = threadIdx.x;
+  if (s < S && flag[s]) st[s].real = 0;
+}
+
+// One batched solve.  Right-hand side: f (real, every shift) or rhs (a
+// complex shift block, one per shift).  Tolerance: tols[s] (host) or tol.
+static int solve(tem_ctx* c, const double* mass, const double* f, const double2* rhs, int S,
+                 const double* shifts, double tol, const double* tols, int maxit, double* x, char* w,
+                 const WorkLayout& L, int* iters, double* relres, cudaStream_t stream) {
   const bool split = c->solver == TEM_SOLVER_SPLIT;
   using T2 = tem::Tile<tem::kTYTwoSweep>;
   using TS = tem::Tile<tem::kTYSplit>;
@@ -613,10 +755,12 @@ static int solve(tem_ctx* c, const double* mass, const double* f, int S, const d
   const int nt = split ? TS::NT : T2::NT;
   double2* Z[2] = {reinterpret_cast<double2*>(w + L.z), reinterpret_cast<double2*>(w + L.z1)};
   double2* P[2] = {reinterpret_cast<double2*>(w + L.p0), reinterpret_cast<double2*>(w + L.p1)};
-  CUtensorMap tmZ[2], tmP[2];
+  CUtensorMap tmZ[2], tmP[2], tmZr[2], tmPr[2];
   for (int q = 0; q < 2; ++q) {
     if (int rc = make_tmap(c, S, Z[q], &tmZ[q], ty)) return rc;
     if (int rc = make_tmap(c, S, P[q], &tmP[q], ty)) return rc;
+    if (int rc = make_tmap(c, S, Z[q], &tmZr[q], ty, true)) return rc;
+    if (int rc = make_tmap(c, S, P[q], &tmPr[q], ty, true)) return rc;
   }
   tem::SweepArgs base{};
   int grid = 0;
@@ -624,6 +768,7 @@ static int solve(tem_ctx* c, const double* mass, const double* f, int S, const d
   base.mass = mass;
   base.x = reinterpret_cast<double2*>(x);
   base.z = Z[0];
+  base.rhs = rhs;
   base.st = reinterpret_cast<tem::ShiftState*>(w + L.st);
   base.ctl = reinterpret_cast<tem::Control*>(w + L.ctl);
   base.part_c = reinterpret_cast<double2*>(w + L.part_c);
@@ -655,27 +800,29 @@ static int solve(tem_ctx* c, const double* mass, const double* f, int S, const d
   auto launch_iter = [&](const Cfg& k, int q, cudaStream_t st_) {
     if (split) {
       if (q == 0)
-        tem::k_sweep<3><<<k.grid, TS::NT, TS::kSmemUpd, st_>>>(k.a1[0], tmP[0], tmZ[0]);
+        tem::k_sweep<3><<<k.grid, TS::NT, TS::kSmemUpd, st_>>>(k.a1[0], tmP[0], tmZ[0], tmPr[0], tmZr[0]);
       else
-        tem::k_sweep<4><<<k.grid, TS::NT, TS::kSmemDirap, st_>>>(k.a1[1], tmP[1], tmZ[1]);
-      tem::k_delta<false><<<k.grid, TS::NT, TS::kSmemDelta, st_>>>(k.a2[q], tmZ[1 - q]);
+        tem::k_sweep<4><<<k.grid, TS::NT, TS::kSmemDirap, st_>>>(k.a1[1], tmP[1], tmZ[1], tmPr[1], tmZr[1]);
+      tem::k_delta<false><<<k.grid, TS::NT, TS::kSmemDelta, st_>>>(k.a2[q], tmZ[1 - q], tmZr[1 - q]);
     } else {
-      tem::k_sweep<1><<<k.grid, T2::NT, T2::kSmemDirap, st_>>>(k.a1[q], tmP[q], tmZ[0]);
-      tem::k_sweep<2><<<k.grid, T2::NT, T2::kSmemDirect, st_>>>(k.a2[q], tmP[1 - q], tmP[1 - q]);
+      tem::k_sweep<1><<<k.grid, T2::NT, T2::kSmemDirap, st_>>>(k.a1[q], tmP[q], tmZ[0], tmP[q], tmZ[0]);
+      tem::k_sweep<2><<<k.grid, T2::NT, T2::kSmemDirect, st_>>>(k.a2[q], tmP[1 - q], tmP[1 - q], tmP[1 - q],
+                                                                  tmP[1 - q]);
     }
   };
   // graphs of kChunk iterations, cached per (slots, z-chunks) for these buffers and this scheme
-  const std::vector<const void*> key = {mass, x, w, f, reinterpret_cast<const void*>((uintptr_t)c->solver)};
-  if (c->graph_key != key || c->graph_S != S) {
-    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+  const std::vector<const void*> key = {mass, x, w, f, rhs, reinterpret_cast<const void*>((uintptr_t)c->solver),
+                                        reinterpret_cast<const void*>((uintptr_t)S)};
+  if (!c->graphs.count(key) && c->graphs.size() >= 4) {
+    for (auto& set : c->graphs)
+      for (auto& kv : set.second) cudaGraphExecDestroy(kv.second);
     c->graphs.clear();
-    c->graph_key = key;
-    c->graph_S = S;
   }
+  auto& gset = c->graphs[key];
   auto get_graph = [&](const Cfg& k, int nslot, cudaGraphExec_t* out) -> int {
     const long long id = (long long)nslot * 4096 + k.a1[0].nzc;
-    auto it = c->graphs.find(id);
-    if (it != c->graphs.end()) {
+    auto it = gset.find(id);
+    if (it != gset.end()) {
       *out = it->second;
       return TEM_OK;
     }
@@ -687,34 +834,43 @@ static int solve(tem_ctx* c, const double* mass, const double* f, int S, const d
     cudaError_t e = cudaGraphInstantiate(&ex, gr, 0);
     cudaGraphDestroy(gr);
     if (e != cudaSuccess) return fail(TEM_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
-    c->graphs[id] = ex;
+    gset[id] = ex;
     *out = ex;
     return TEM_OK;
   };
 
   // per-shift state + control (host -> device, small)
   std::vector<tem::ShiftState> st(S);
+  bool any_real = false;
   for (int s = 0; s < S; ++s) {
     memset(&st[s], 0, sizeof(tem::ShiftState));
     st[s].s = make_double2(shifts[2 * s], shifts[2 * s + 1]);
+    st[s].tol = tols ? tols[s] : tol;
+    st[s].real = (split && c->real_arith && shifts[2 * s + 1] == 0.0) ? 1 : 0;
+    any_real |= st[s].real != 0;
   }
   tem::Control ctl{};
-  ctl.tol = tol;
   TEM_CUDA(cudaMemcpyAsync(base.st, st.data(), sizeof(tem::ShiftState) * S, cudaMemcpyHostToDevice, stream));
   TEM_CUDA(cudaMemcpyAsync(base.ctl, &ctl, sizeof(tem::Control), cudaMemcpyHostToDevice, stream));
 
-  cudaEvent_t ev0, ev1;
-  TEM_CUDA(cudaEventCreate(&ev0));
-  TEM_CUDA(cudaEventCreate(&ev1));
-  TEM_CUDA(cudaEventRecord(ev0, stream));
+  TEM_CUDA(cudaEventRecord(c->ev0, stream));
+  long long launches = 0;
+  if (rhs && any_real) {   // a real shift with a complex right-hand side runs in complex arithmetic
+    int* flags = reinterpret_cast<int*>(w + L.flags);
+    TEM_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * TEM_MAX_SHIFTS, stream));
+    k_rhs_imag<<<dim3(64, S), 256, 0, stream>>>(rhs, 3 * c->g.Nn, flags);
+    k_real_mask<<<1, 32, 0, stream>>>(base.st, flags, S);
+    TEM_CUDA(cudaGetLastError());
+    launches += 2;
+  }
   const int vec_grid = S * std::max(1, std::min(64, (int)((3 * c->g.Nn + 255) / 256)));
   k_init<<<vec_grid, 256, 0, stream>>>(base, P[0], P[1], split ? Z[1] : nullptr, f);
   TEM_CUDA(cudaGetLastError());
-  long long launches = 1;
+  launches += 1;
   int nslot = S;
   Cfg cfg = make_cfg(nslot);
   if (split) {
-    tem::k_delta<true><<<cfg.grid, TS::NT, TS::kSmemDelta, stream>>>(cfg.a2[0], tmZ[0]);   // delta_0
+    tem::k_delta<true><<<cfg.grid, TS::NT, TS::kSmemDelta, stream>>>(cfg.a2[0], tmZ[0], tmZr[0]);   // delta_0
     TEM_CUDA(cudaGetLastError());
     launches += 1;
   }
@@ -753,11 +909,16 @@ static int solve(tem_ctx* c, const double* mass, const double* f, int S, const d
   }
   if (split) {
     k_xfix<<<vec_grid, 256, 0, stream>>>(base, P[1]);
-    TEM_CUDA(cudaGetLastError());
     launches += 1;
+    if (any_real) {   // real-layout x of real shifts -> complex ABI layout (Z[0] as scratch)
+      k_real_out<<<vec_grid, 256, 0, stream>>>(base, Z[0], 0);
+      k_real_out<<<vec_grid, 256, 0, stream>>>(base, Z[0], 1);
+      launches += 2;
+    }
+    TEM_CUDA(cudaGetLastError());
   }
-  TEM_CUDA(cudaEventRecord(ev1, stream));
-  return finish_solve(c, S, st, base.st, ev0, ev1, stream, launches, grid, nt, iters, relres);
+  TEM_CUDA(cudaEventRecord(c->ev1, stream));
+  return finish_solve(c, S, st, base.st, stream, launches, grid, nt, iters, relres);
 }
 
 int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const double* shifts,
@@ -766,10 +927,28 @@ int tem_cocg_solve(tem_ctx* c, const double* mass, const double* f, int S, const
   if (!c || !mass || !f || !shifts || !x || !work) return fail(TEM_EINVAL, "tem_cocg_solve: null pointer");
   if (int rc = check_S(S)) return rc;
   if (!(tol > 0.0) || maxit < 1) return fail(TEM_EINVAL, "tem_cocg_solve: need tol > 0, maxit >= 1");
+  if (int rc = check_device(c)) return rc;
   const WorkLayout L = work_layout(c, S);
   if (work_bytes < L.total) return fail(TEM_EINVAL, "tem_cocg_solve: workspace too small");
-  return solve(c, mass, f, S, shifts, tol, maxit, x, static_cast<char*>(work), L, iters, relres,
-               (cudaStream_t)stream_);
+  return solve(c, mass, f, nullptr, S, shifts, tol, nullptr, maxit, x, static_cast<char*>(work), L, iters,
+               relres, (cudaStream_t)stream_);
+}
+
+int tem_cocg_solve_rhs(tem_ctx* c, const double* mass, const double* rhs, int S, const double* shifts,
+                       const double* tols, int maxit, double* x, void* work, size_t work_bytes, int* iters,
+                       double* relres, void* stream_) {
+  if (!c || !mass || !rhs || !shifts || !tols || !x || !work)
+    return fail(TEM_EINVAL, "tem_cocg_solve_rhs: null pointer");
+  if (int rc = check_S(S)) return rc;
+  if (int rc = check_device(c)) return rc;
+  if (maxit < 1) return fail(TEM_EINVAL, "tem_cocg_solve_rhs: need maxit >= 1");
+  for (int s = 0; s < S; ++s)
+    if (!(tols[s] > 0.0)) return fail(TEM_EINVAL, "tem_cocg_solve_rhs: need tols[s] > 0");
+  if (rhs == x) return fail(TEM_EINVAL, "tem_cocg_solve_rhs: rhs and x must not alias");
+  const WorkLayout L = work_layout(c, S);
+  if (work_bytes < L.total) return fail(TEM_EINVAL, "tem_cocg_solve_rhs: workspace too small");
+  return solve(c, mass, nullptr, reinterpret_cast<const double2*>(rhs), S, shifts, 0.0, tols, maxit, x,
+               static_cast<char*>(work), L, iters, relres, (cudaStream_t)stream_);
 }
 
 int tem_set_solver(tem_ctx* c, int solver) {
@@ -788,43 +967,65 @@ int tem_last_solve_stats(const tem_ctx* c, tem_solve_stats* out) {
   return TEM_OK;
 }
 
-static int ensure_scratch(tem_ctx* c, size_t bytes) {
-  if (c->scratch_bytes >= bytes) return TEM_OK;
-  if (c->scratch) cudaFree(c->scratch);
-  c->scratch = nullptr;
-  c->scratch_bytes = 0;
-  TEM_CUDA(cudaMalloc(&c->scratch, bytes));
-  c->scratch_bytes = bytes;
+// Small host arrays (residues, receivers) reach the device through a
+// context-owned pinned staging buffer: the copy is asynchronous on the
+// caller's stream and the pageable caller array may be reused on return.
+// The staging buffer is rewritten only after the previous copy out of it
+// has completed (stage_ev); the device scratch is stream-ordered (calls on
+// one context are issued on one stream, include/tem_b200.h).
+static int stage_to_device(tem_ctx* c, const void* const* src, const size_t* bytes, int n, cudaStream_t stream) {
+  size_t total = 0;
+  for (int i = 0; i < n; ++i) total += align_up(bytes[i], 256);
+  if (c->stage_ev) TEM_CUDA(cudaEventSynchronize(c->stage_ev));
+  if (c->pin_bytes < total) {
+    if (c->pin) cudaFreeHost(c->pin);
+    c->pin = nullptr;
+    c->pin_bytes = 0;
+    TEM_CUDA(cudaMallocHost(&c->pin, total));
+    c->pin_bytes = total;
+  }
+  if (c->scratch_bytes < total) {
+    if (c->scratch) {
+      TEM_CUDA(cudaStreamSynchronize(stream));   // a queued kernel may still read the old scratch
+      cudaFree(c->scratch);
+    }
+    c->scratch = nullptr;
+    c->scratch_bytes = 0;
+    TEM_CUDA(cudaMalloc(&c->scratch, total));
+    c->scratch_bytes = total;
+  }
+  size_t o = 0;
+  for (int i = 0; i < n; ++i) {
+    memcpy(static_cast<char*>(c->pin) + o, src[i], bytes[i]);
+    o += align_up(bytes[i], 256);
+  }
+  TEM_CUDA(cudaMemcpyAsync(c->scratch, c->pin, total, cudaMemcpyHostToDevice, stream));
+  TEM_CUDA(cudaEventRecord(c->stage_ev, stream));
   return TEM_OK;
 }
 
-int tem_synthesize(tem_ctx* c, int S, int K, const double* residues, const int* is_pair,
-                   const double* x, double* u, void* stream_) {
-  if (!c || !residues || !is_pair || !x || !u) return fail(TEM_EINVAL, "tem_synthesize: null pointer");
-  if (int rc = check_S(S)) return rc;
-  if (K < 1) return fail(TEM_EINVAL, "tem_synthesize: K must be >= 1");
+// u = sum_s w_s Re(res[k][s] x_s), residues [K][S] complex on the host.
+static int synth(tem_ctx* c, int S, int K, const double* residues, const int* is_pair, const double2* x,
+                 double* u, cudaStream_t stream) {
   const size_t res_bytes = (size_t)K * S * sizeof(double2);
   const size_t smem = res_bytes;
   if (smem > 200 * 1024) return fail(TEM_EINVAL, "tem_synthesize: K*S too large for shared memory");
-  // scratch: residues [K][S] complex, then weights [S]
-  if (int rc = ensure_scratch(c, res_bytes + TEM_MAX_SHIFTS * sizeof(double))) return rc;
-  cudaStream_t stream = (cudaStream_t)stream_;
-  std::vector<double> wts(S);
+  double wts[TEM_MAX_SHIFTS];
   for (int s = 0; s < S; ++s) wts[s] = is_pair[s] ? 2.0 : 1.0;
+  const void* src[2] = {residues, wts};
+  const size_t bytes[2] = {res_bytes, S * sizeof(double)};
+  if (int rc = stage_to_device(c, src, bytes, 2, stream)) return rc;
   char* sc = static_cast<char*>(c->scratch);
-  TEM_CUDA(cudaMemcpyAsync(sc, residues, res_bytes, cudaMemcpyHostToDevice, stream));
-  TEM_CUDA(cudaMemcpyAsync(sc + res_bytes, wts.data(), S * sizeof(double), cudaMemcpyHostToDevice, stream));
+  const double2* res_d = reinterpret_cast<const double2*>(sc);
+  const double* w_d = reinterpret_cast<const double*>(sc + align_up(res_bytes, 256));
   const long long nslots = 3 * c->g.Nn;
   const int block = 128;
   const int grid = (int)std::min<long long>((nslots + block - 1) / block, (long long)c->num_sms * 16);
-  const double2* res_d = reinterpret_cast<const double2*>(sc);
-  const double* w_d = reinterpret_cast<const double*>(sc + res_bytes);
-  const double2* xd = reinterpret_cast<const double2*>(x);
 #define TEM_SYNTH(SM)                                                                      \
   do {                                                                                     \
     if (smem > 48 * 1024)                                                                  \
       TEM_CUDA(cudaFuncSetAttribute(k_synth<SM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    k_synth<SM><<<grid, block, smem, stream>>>(c->g, S, K, res_d, w_d, xd, u);             \
+    k_synth<SM><<<grid, block, smem, stream>>>(c->g, S, K, res_d, w_d, x, u);              \
   } while (0)
   if (S <= 8) TEM_SYNTH(8);
   else if (S <= 16) TEM_SYNTH(16);
@@ -832,49 +1033,314 @@ int tem_synthesize(tem_ctx* c, int S, int K, const double* residues, const int* 
   else TEM_SYNTH(32);
 #undef TEM_SYNTH
   TEM_CUDA(cudaGetLastError());
-  // synchronise so the pageable host buffers above are not reused early
-  TEM_CUDA(cudaStreamSynchronize(stream));
   return TEM_OK;
+}
+
+int tem_synthesize(tem_ctx* c, int S, int K, const double* residues, const int* is_pair,
+                   const double* x, double* u, void* stream_) {
+  if (!c || !residues || !is_pair || !x || !u) return fail(TEM_EINVAL, "tem_synthesize: null pointer");
+  if (int rc = check_S(S)) return rc;
+  if (int rc = check_device(c)) return rc;
+  if (K < 1) return fail(TEM_EINVAL, "tem_synthesize: K must be >= 1");
+  return synth(c, S, K, residues, is_pair, reinterpret_cast<const double2*>(x), u, (cudaStream_t)stream_);
 }
 
 int tem_curl_z(tem_ctx* c, int K, const double* u, int R, const int* receivers, double* out, void* stream_) {
   if (!c || !u || !receivers || !out) return fail(TEM_EINVAL, "tem_curl_z: null pointer");
   if (K < 1 || R < 1) return fail(TEM_EINVAL, "tem_curl_z: need K >= 1, R >= 1");
+  if (int rc = check_device(c)) return rc;
   for (int r = 0; r < R; ++r) {
     const int i = receivers[3 * r], j = receivers[3 * r + 1], k = receivers[3 * r + 2];
     if (i < 0 || i >= c->g.n[0] || j < 0 || j >= c->g.n[1] || k < 0 || k > c->g.n[2])
       return fail(TEM_EINVAL, "tem_curl_z: receiver " + std::to_string(r) + " outside the grid");
   }
-  const size_t rec_bytes = (size_t)3 * R * sizeof(int);
-  if (int rc = ensure_scratch(c, rec_bytes)) return rc;
   cudaStream_t stream = (cudaStream_t)stream_;
-  TEM_CUDA(cudaMemcpyAsync(c->scratch, receivers, rec_bytes, cudaMemcpyHostToDevice, stream));
+  const void* src[1] = {receivers};
+  const size_t bytes[1] = {(size_t)3 * R * sizeof(int)};
+  if (int rc = stage_to_device(c, src, bytes, 1, stream)) return rc;
   const int n = K * R, block = 256;
   k_curl_z<<<(n + block - 1) / block, block, 0, stream>>>(c->g, K, R, static_cast<const int*>(c->scratch),
                                                           u, out);
   TEM_CUDA(cudaGetLastError());
-  TEM_CUDA(cudaStreamSynchronize(stream));   // the host receiver list may be reused on return
+  return TEM_OK;
+}
+
+// ------------------------------------------------------------ forward
+// tem_forward: solve, synthesise, and (opts->max_refine > 0) refine until
+// the channels are converged (reading R13).
+struct FwdLayout {
+  size_t cocg, r, d, part, out, total;
+  int nblk;
+};
+
+static FwdLayout fwd_layout(const tem_ctx* c, int S, int K) {
+  FwdLayout L{};
+  const size_t vec = (size_t)3 * c->g.Nn * S * sizeof(double2);
+  L.nblk = 2 * std::max(1, c->num_sms);
+  const size_t rows = (size_t)std::max(4 * S, K);
+  size_t o = 0;
+  L.cocg = o;  o = align_up(o + work_layout(c, S).total, 256);
+  L.r = o;     o = align_up(o + vec, 256);
+  L.d = o;     o = align_up(o + vec, 256);
+  L.part = o;  o = align_up(o + rows * L.nblk * sizeof(double), 256);
+  L.out = o;   o = align_up(o + rows * sizeof(double), 256);
+  L.total = o;
+  return L;
+}
+
+// device rows -> host: out[row] = sum_b part[row][b]
+static int rows_to_host(tem_ctx* c, const double* part, int nrow, int ncol, double* dev_out, double* host,
+                        cudaStream_t stream) {
+  k_rows_sum<<<(nrow + 7) / 8, 256, 0, stream>>>(part, nrow, ncol, dev_out);
+  TEM_CUDA(cudaGetLastError());
+  TEM_CUDA(cudaMemcpyAsync(host, dev_out, nrow * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  TEM_CUDA(cudaStreamSynchronize(stream));
+  return TEM_OK;
+}
+
+static int resid_dd(tem_ctx* c, const double* mass, const double* f, int S, const double* shifts,
+                    const std::vector<int>& list, const double2* x, double2* r, const FwdLayout& L, char* w,
+                    std::vector<double>& res2, cudaStream_t stream) {
+  tem::ResidArgs A{};
+  A.g = c->g;
+  A.mass = mass;
+  A.f = f;
+  A.x = x;
+  A.r = r;
+  A.part = reinterpret_cast<double*>(w + L.part);
+  const int n = (int)list.size();
+  for (int y = 0; y < n; ++y) {
+    A.list[y] = list[y];
+    A.shifts[y] = make_double2(shifts[2 * list[y]], shifts[2 * list[y] + 1]);
+  }
+  tem::k_resid_dd<<<dim3(L.nblk, n), 256, 0, stream>>>(A);
+  TEM_CUDA(cudaGetLastError());
+  res2.assign(n, 0.0);
+  return rows_to_host(c, A.part, n, L.nblk, reinterpret_cast<double*>(w + L.out), res2.data(), stream);
+}
+
+static int forward(tem_ctx* c, const double* mass, const double* f, int S, const double* shifts, int K,
+                   const double* residues, const int* is_pair, const tem_forward_opts& o, double* x, double* u,
+                   char* w, const FwdLayout& L, int* iters, double* relres, tem_forward_stats* fst,
+                   cudaStream_t stream) {
+  const WorkLayout WL = work_layout(c, S);
+  char* wc = w + L.cocg;
+  double2* xc = reinterpret_cast<double2*>(x);
+  double2* r = reinterpret_cast<double2*>(w + L.r);
+  double2* d = reinterpret_cast<double2*>(w + L.d);
+  const size_t vec1 = (size_t)3 * c->g.Nn * sizeof(double2);
+  std::vector<int> it(S, 0), it1(S, 0);
+  std::vector<double> rr(S, 0.0);
+  tem_forward_stats F{};
+  int rc_solve = solve(c, mass, f, nullptr, S, shifts, o.tol, nullptr, o.maxit, x, wc, WL, it.data(), rr.data(),
+                       stream);
+  if (rc_solve == TEM_ECUDA || rc_solve == TEM_EINVAL) return rc_solve;
+  std::string solve_msg = g_last_error;
+  F.shift_iterations = c->stats.shift_iterations;
+  F.loop_ms = c->stats.loop_ms;
+  F.initial_shift_iterations = c->stats.shift_iterations;
+  const double fnorm = c->last_fnorm;
+  if (int rc = synth(c, S, K, residues, is_pair, xc, u, stream)) return rc;
+  F.channel_bound = -1.0;   // not estimated (no refinement)
+  if (o.max_refine > 0 && rc_solve == TEM_OK && fnorm > 0.0) {
+    // ||u_k||_M per channel (the yardstick of the channel-aware rule)
+    double* part = reinterpret_cast<double*>(w + L.part);
+    double* dout = reinterpret_cast<double*>(w + L.out);
+    k_channel_mnorm<<<dim3(L.nblk, K), 256, 0, stream>>>(3 * c->g.Nn, mass, u, part);
+    TEM_CUDA(cudaGetLastError());
+    std::vector<double> unorm(K);
+    if (int rc = rows_to_host(c, part, K, L.nblk, dout, unorm.data(), stream)) return rc;
+    for (auto& v : unorm) v = sqrt(v);
+    std::vector<int> list(S);
+    for (int s = 0; s < S; ++s) list[s] = s;
+    std::vector<double> res_prev(S), res_now;
+    if (int rc = resid_dd(c, mass, f, S, shifts, list, xc, r, L, w, res_now, stream)) return rc;
+    for (int s = 0; s < S; ++s) res_prev[s] = sqrt(res_now[s]);
+    // est[s][k]: estimated remaining error of shift s in channel k (relative M-norm)
+    std::vector<double> est((size_t)S * K, 0.0);
+    std::vector<double> tols(S);
+    for (int round = 1; round <= o.max_refine; ++round) {
+      // right-hand sides: r for the refined shifts (written by resid_dd), 0 for the others
+      std::vector<char> on(S, 0);
+      for (int s : list) on[s] = 1;
+      for (int s = 0; s < S; ++s) {
+        tols[s] = o.refine_tol;
+        if (!on[s]) TEM_CUDA(cudaMemsetAsync(r + (size_t)s * 3 * c->g.Nn, 0, vec1, stream));
+      }
+      const int rc2 = solve(c, mass, nullptr, r, S, shifts, 0.0, tols.data(), o.maxit, reinterpret_cast<double*>(d),
+                            wc, WL, it1.data(), nullptr, stream);
+      if (rc2 == TEM_ECUDA || rc2 == TEM_EINVAL) return rc2;
+      if (rc2 != TEM_OK && rc_solve == TEM_OK) {
+        rc_solve = rc2;
+        solve_msg = g_last_error;
+      }
+      for (int s = 0; s < S; ++s) it[s] += it1[s];
+      F.shift_iterations += c->stats.shift_iterations;
+      F.loop_ms += c->stats.loop_ms;
+      F.refine_rounds = round;
+      // x += d, and the M-weighted statistics of d
+      tem::UpdateArgs U{};
+      U.Nn = c->g.Nn;
+      U.mass = mass;
+      U.x = xc;
+      U.d = d;
+      U.part = part;
+      const int n = (int)list.size();
+      for (int y = 0; y < n; ++y) U.list[y] = list[y];
+      tem::k_refine_update<<<dim3(L.nblk, n), 256, 0, stream>>>(U);
+      TEM_CUDA(cudaGetLastError());
+      std::vector<double> dst(4 * n);
+      if (int rc = rows_to_host(c, part, 4 * n, L.nblk, dout, dst.data(), stream)) return rc;
+      if (int rc = resid_dd(c, mass, f, S, shifts, list, xc, r, L, w, res_now, stream)) return rc;
+      std::vector<int> next;
+      for (int y = 0; y < n; ++y) {
+        const int s = list[y];
+        const double rho_after = sqrt(res_now[y]);
+        // contraction of this round ~ the residual ratio it achieved (times a
+        // safety factor for the error-to-residual amplification, R13)
+        const double contr = std::min(1.0, o.safety * rho_after / std::max(res_prev[s], 1e-300));
+        const double wgt = is_pair[s] ? 2.0 : 1.0;
+        double worst = 0.0;
+        for (int k = 0; k < K; ++k) {
+          const double ar = residues[2 * ((size_t)k * S + s)], ai = residues[2 * ((size_t)k * S + s) + 1];
+          const double q = ar * ar * dst[4 * y] + ai * ai * dst[4 * y + 1] - 2.0 * ar * ai * dst[4 * y + 2];
+          const double dk = wgt * sqrt(std::max(q, 0.0)) / std::max(unorm[k], 1e-300);   // |last correction|
+          est[(size_t)s * K + k] = dk * contr;
+          worst = std::max(worst, dk * contr);
+        }
+        res_prev[s] = rho_after;
+        if (worst > o.channel_tol / S) next.push_back(s);
+      }
+      double bound = 0.0;
+      for (int k = 0; k < K; ++k) {
+        double b = 0.0;
+        for (int s = 0; s < S; ++s) b += est[(size_t)s * K + k];
+        bound = std::max(bound, b);
+      }
+      F.channel_bound = bound;
+      list = next;
+      if (bound <= o.channel_tol || list.empty()) break;
+    }
+    for (int s = 0; s < S; ++s) rr[s] = res_prev[s] / fnorm;
+    if (int rc = synth(c, S, K, residues, is_pair, xc, u, stream)) return rc;
+  }
+  double rmax = 0.0;
+  for (int s = 0; s < S; ++s) {
+    if (iters) iters[s] = it[s];
+    if (relres) relres[s] = rr[s];
+    rmax = std::max(rmax, rr[s]);
+  }
+  F.relres_max = rmax;
+  if (fst) *fst = F;
+  c->fstats = F;
+  if (rc_solve != TEM_OK) return fail(rc_solve, solve_msg);
+  return TEM_OK;
+}
+
+static int check_opts(const tem_forward_opts* o) {
+  if (!(o->tol > 0.0) || o->maxit < 1 || o->max_refine < 0)
+    return fail(TEM_EINVAL, "tem_forward: need tol > 0, maxit >= 1, max_refine >= 0");
+  if (o->max_refine > 0 && !(o->refine_tol > 0.0 && o->refine_tol < 1.0 && o->channel_tol > 0.0 && o->safety >= 1.0))
+    return fail(TEM_EINVAL, "tem_forward: need 0 < refine_tol < 1, channel_tol > 0, safety >= 1");
+  return TEM_OK;
+}
+
+size_t tem_forward_workspace_bytes(const tem_ctx* c, int S, int K) {
+  if (!c || S < 1 || S > TEM_MAX_SHIFTS || K < 1) return 0;
+  return fwd_layout(c, S, K).total;
+}
+
+void tem_forward_default_opts(tem_forward_opts* o) {
+  if (!o) return;
+  o->tol = 1e-10;
+  o->maxit = 200000;
+  o->max_refine = 0;
+  o->refine_tol = 1e-6;
+  o->channel_tol = 1e-8;
+  o->safety = 100.0;
+}
+
+int tem_forward(tem_ctx* c, const double* mass, const double* f, int S, const double* shifts, int K,
+                const double* residues, const int* is_pair, const tem_forward_opts* opts, double* x, double* u,
+                void* work, size_t work_bytes, int* iters, double* relres, tem_forward_stats* fst,
+                void* stream) {
+  if (!c || !mass || !f || !shifts || !residues || !is_pair || !opts || !x || !u || !work)
+    return fail(TEM_EINVAL, "tem_forward: null pointer");
+  if (int rc = check_S(S)) return rc;
+  if (int rc = check_device(c)) return rc;
+  if (K < 1) return fail(TEM_EINVAL, "tem_forward: K must be >= 1");
+  if (int rc = check_opts(opts)) return rc;
+  const FwdLayout L = fwd_layout(c, S, K);
+  if (work_bytes < L.total) return fail(TEM_EINVAL, "tem_forward: workspace too small");
+  return forward(c, mass, f, S, shifts, K, residues, is_pair, *opts, x, u, static_cast<char*>(work), L, iters,
+                 relres, fst, (cudaStream_t)stream);
+}
+
+int tem_residual(tem_ctx* c, const double* mass, const double* f, int S, const double* shifts, const double* x,
+                 double* r, double* rnorm, void* stream_) {
+  if (!c || !mass || !f || !shifts || !x || !r) return fail(TEM_EINVAL, "tem_residual: null pointer");
+  if (int rc = check_S(S)) return rc;
+  if (int rc = check_device(c)) return rc;
+  if (x == r) return fail(TEM_EINVAL, "tem_residual: x and r must not alias");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const int nblk = 2 * std::max(1, c->num_sms);
+  const size_t need = ((size_t)S * nblk + TEM_MAX_SHIFTS) * sizeof(double);
+  if (c->red_bytes < need) {
+    if (c->red) {
+      TEM_CUDA(cudaStreamSynchronize(stream));
+      cudaFree(c->red);
+    }
+    c->red = nullptr;
+    c->red_bytes = 0;
+    TEM_CUDA(cudaMalloc(&c->red, need));
+    c->red_bytes = need;
+  }
+  tem::ResidArgs A{};
+  A.g = c->g;
+  A.mass = mass;
+  A.f = f;
+  A.x = reinterpret_cast<const double2*>(x);
+  A.r = reinterpret_cast<double2*>(r);
+  A.part = static_cast<double*>(c->red);
+  for (int y = 0; y < S; ++y) {
+    A.list[y] = y;
+    A.shifts[y] = make_double2(shifts[2 * y], shifts[2 * y + 1]);
+  }
+  tem::k_resid_dd<<<dim3(nblk, S), 256, 0, stream>>>(A);
+  TEM_CUDA(cudaGetLastError());
+  if (!rnorm) return TEM_OK;
+  double* dout = static_cast<double*>(c->red) + (size_t)S * nblk;
+  std::vector<double> rr(S);
+  if (int rc = rows_to_host(c, A.part, S, nblk, dout, rr.data(), stream)) return rc;
+  for (int y = 0; y < S; ++y) rnorm[y] = sqrt(rr[y]);
+  return TEM_OK;
+}
+
+int tem_last_forward_stats(const tem_ctx* c, tem_forward_stats* out) {
+  if (!c || !out) return fail(TEM_EINVAL, "tem_last_forward_stats: null pointer");
+  *out = c->fstats;
   return TEM_OK;
 }
 
 int tem_forward_host(tem_ctx* c, const double* sigma, const double* f, int S, const double* shifts,
-                     int K, const double* residues, const int* is_pair, double tol, int maxit,
+                     int K, const double* residues, const int* is_pair, const tem_forward_opts* opts,
                      double* u, int* iters, double* relres) {
-  if (!c || !sigma || !f || !shifts || !residues || !is_pair || !u)
+  if (!c || !sigma || !f || !shifts || !residues || !is_pair || !opts || !u)
     return fail(TEM_EINVAL, "tem_forward_host: null pointer");
   if (int rc = check_S(S)) return rc;
+  if (int rc = check_device(c)) return rc;
   if (K < 1) return fail(TEM_EINVAL, "tem_forward_host: K must be >= 1");
+  if (int rc = check_opts(opts)) return rc;
   const size_t ncell = (size_t)c->g.n[0] * c->g.n[1] * c->g.n[2];
   const size_t nsl = (size_t)3 * c->g.Nn;
+  const FwdLayout FL = fwd_layout(c, S, K);
   size_t o = 0;
   const size_t o_sig = o;  o = align_up(o + ncell * sizeof(double), 256);
   const size_t o_f = o;    o = align_up(o + nsl * sizeof(double), 256);
   const size_t o_m = o;    o = align_up(o + nsl * sizeof(double), 256);
   const size_t o_x = o;    o = align_up(o + nsl * S * sizeof(double2), 256);
   const size_t o_u = o;    o = align_up(o + (size_t)K * nsl * sizeof(double), 256);
-  const size_t o_w = o;
-  const size_t wbytes = tem_cocg_workspace_bytes(c, S);
-  o = align_up(o + wbytes, 256);
+  const size_t o_w = o;    o = align_up(o + FL.total, 256);
   if (c->e2e_bytes < o) {
     if (c->e2e) cudaFree(c->e2e);
     c->e2e = nullptr;
@@ -888,16 +1354,14 @@ int tem_forward_host(tem_ctx* c, const double* sigma, const double* f, int S, co
   TEM_CUDA(cudaMemcpyAsync(b + o_sig, sigma, ncell * sizeof(double), cudaMemcpyHostToDevice, stream));
   TEM_CUDA(cudaMemcpyAsync(b + o_f, f, nsl * sizeof(double), cudaMemcpyHostToDevice, stream));
   if (int rc = tem_edge_mass(c, (const double*)(b + o_sig), (double*)(b + o_m), stream)) return rc;
-  const int rc_solve = tem_cocg_solve(c, (const double*)(b + o_m), (const double*)(b + o_f), S, shifts,
-                                      tol, maxit, (double*)(b + o_x), b + o_w, wbytes, iters, relres,
-                                      stream);
-  if (rc_solve == TEM_ECUDA || rc_solve == TEM_EINVAL) return rc_solve;
-  const std::string solve_msg = g_last_error;
-  if (int rc = tem_synthesize(c, S, K, residues, is_pair, (const double*)(b + o_x), (double*)(b + o_u), stream))
-    return rc;
+  const int rc_fwd = forward(c, (const double*)(b + o_m), (const double*)(b + o_f), S, shifts, K, residues, is_pair,
+                             *opts, (double*)(b + o_x), (double*)(b + o_u), b + o_w, FL, iters, relres, nullptr,
+                             stream);
+  if (rc_fwd == TEM_ECUDA || rc_fwd == TEM_EINVAL) return rc_fwd;
+  const std::string msg = g_last_error;
   TEM_CUDA(cudaMemcpyAsync(u, b + o_u, (size_t)K * nsl * sizeof(double), cudaMemcpyDeviceToHost, stream));
   TEM_CUDA(cudaStreamSynchronize(stream));
-  if (rc_solve != TEM_OK) return fail(rc_solve, solve_msg);
+  if (rc_fwd != TEM_OK) return fail(rc_fwd, msg);
   return TEM_OK;
 }
 

@@ -25,6 +25,12 @@ struct Grid {
   int n[3];               // cells per axis
   long long st[3];        // node strides: 1, nx+1, (nx+1)(ny+1)
   long long Nn;           // nodes
+  // Real-arithmetic shifts keep their COCG vectors as fp64 edge vectors with
+  // the node rows padded to an even length px (so every TMA global stride is
+  // a multiple of 16 B): slot c * NnP + (k (ny+1) + j) px + i, stored at the
+  // start of the shift's complex slot region (8 * 3 NnP <= 16 * 3 Nn bytes).
+  int px;                 // nx + 1 rounded up to even
+  long long NnP;          // px (ny+1) (nz+1)
   const double* ih[3];    // 1 / h_a[i], i < n_a                     (device)
   const double* hdm[3];   // hdual_a[i] / mu0, i = 0..n_a             (device)
 };
@@ -59,6 +65,57 @@ __device__ __forceinline__ double2 crcp(double2 b) {
   double n;
   return crcp(b, n);
 }
+__device__ __forceinline__ double2 csq(double2 a) { return make_double2(fma(a.x, a.x, -a.y * a.y), 2.0 * a.x * a.y); }
+__device__ __forceinline__ double cabs2(double2 a) { return fma(a.x, a.x, a.y * a.y); }
+
+// The same operations on real values: a shift with a real pole (footnote to
+// eq:rmj) has a real SPD system K + s M and a real right-hand side,
+// so its COCG runs in real arithmetic (8 B per value, a quarter of the FP64
+// work).  Kernels are written once over the value type V = double2 | double.
+__device__ __forceinline__ double cadd(double a, double b) { return a + b; }
+__device__ __forceinline__ double csub(double a, double b) { return a - b; }
+__device__ __forceinline__ double cscale(double s, double a) { return s * a; }
+__device__ __forceinline__ double cmul(double a, double b) { return a * b; }
+__device__ __forceinline__ double cfma(double b, double c, double a) { return fma(b, c, a); }
+__device__ __forceinline__ double cdiv(double a, double b) { return a / b; }
+__device__ __forceinline__ double csq(double a) { return a * a; }
+__device__ __forceinline__ double cabs2(double a) { return a * a; }
+__device__ __forceinline__ double crcp(double b, double& n) {
+  n = b * b;
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+  r = fma(r, fma(-b, r, 1.0), r);
+  return fma(r, fma(-b, r, 1.0), r);
+}
+
+// acc + s * a for a real scalar s (component-wise fma)
+__device__ __forceinline__ double2 sfma(double s, double2 a, double2 acc) {
+  return make_double2(fma(s, a.x, acc.x), fma(s, a.y, acc.y));
+}
+__device__ __forceinline__ double sfma(double s, double a, double acc) { return fma(s, a, acc); }
+
+template <typename V>
+struct VT;
+template <>
+struct VT<double2> {
+  static constexpr bool kReal = false;
+  __device__ __forceinline__ static double2 zero() { return make_double2(0.0, 0.0); }
+  __device__ __forceinline__ static double2 from(double2 v) { return v; }     // scalar state -> V
+  __device__ __forceinline__ static double2 cplx(double2 v) { return v; }     // V -> complex
+  __device__ __forceinline__ static double2 make(double re, double im) { return make_double2(re, im); }
+  __device__ __forceinline__ static double re(double2 v) { return v.x; }
+  __device__ __forceinline__ static double im(double2 v) { return v.y; }
+};
+template <>
+struct VT<double> {
+  static constexpr bool kReal = true;
+  __device__ __forceinline__ static double zero() { return 0.0; }
+  __device__ __forceinline__ static double from(double2 v) { return v.x; }
+  __device__ __forceinline__ static double2 cplx(double v) { return make_double2(v, 0.0); }
+  __device__ __forceinline__ static double make(double re, double) { return re; }
+  __device__ __forceinline__ static double re(double v) { return v; }
+  __device__ __forceinline__ static double im(double) { return 0.0; }
+};
 
 // Face weights of the four faces around edge (A, pos): W_d(m), W_d(m-e_b), W_b(m), W_b(m-e_d).
 struct EdgeWeights {

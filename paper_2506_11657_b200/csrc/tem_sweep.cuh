@@ -76,14 +76,14 @@ struct ShiftState {
   double2 dm0;          // split solver: s z_0^T M z_0 (mass part of delta_0, from k_init)
   double fnorm;     // ||f||_2
   double relres;    // ||r||_2 / ||f||_2
+  double tol;       // stopping tolerance of this shift (relative residual)
   int active;
   int iters;
   int status;       // 0 running, 1 converged, 2 breakdown
-  int xlag;         // split solver: x misses alpha p of the last iteration (fixed at the end)
+  int real;         // 1: real shift and real right-hand side -> real arithmetic (split scheme)
 };
 
 struct Control {
-  double tol;
   int n_active;           // number of active shifts
   unsigned int ticket[8];
   int list[32];           // the active shifts, compacted (first n_active entries)
@@ -102,6 +102,7 @@ struct SweepArgs {
   const double2* pold;         // MODE 4: p_{i-1} (own values)
   ShiftState* st;              // [S]
   Control* ctl;
+  const double2* rhs;          // k_init: per-shift right-hand sides (shift block), or NULL (f for all)
   double2* part_c;             // [gridDim]
   double* part_r;              // [gridDim]
   double* part;                // MODE 3, 4, k_delta: [kSplitPart][pstride] per-CTA partial sums
@@ -158,6 +159,7 @@ __device__ __forceinline__ void tma_tile(void* dst, const CUtensorMap* tm, int c
 // do not displace the plane tiles and halo rows still to be re-read
 // (measured: split pass 1 odd -4%).
 __device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(double* p, double v) { __stcs(p, v); }
 
 // q mod n for q >= -8n (ring slots of plane sets; sets start at kb - 2 >= -2)
 __device__ __forceinline__ int pmod(int q, int n) { return (int)((unsigned)(q + 8 * n) % (unsigned)n); }
@@ -275,24 +277,24 @@ __device__ __forceinline__ Column make_column(const Grid& g, int tx0, int ty0) {
 // values: each face circulation F is formed once, scaled by its weight
 // W = hdual/(mu0 A) (G = W F), and the edges combine G's with the incidence
 // signs of K = T^T W T.
+template <typename V>
 struct Edge3 {
-  double2 q[3], p[3];
+  V q[3], p[3];
   double kd[3];
   bool f[3];
 };
 
-// PITCH = row pitch of the tiles (in double2), c0 = index of the node in them.
-template <int PITCH>
+// PITCH = row pitch of the tiles (in V), c0 = index of the node in them.
+template <int PITCH, typename V>
 __device__ __forceinline__ void stencil3p(const Grid& g, const Column& C, int c0, int k, double ihz,
-                                          double ihzm, double hdz, const double2* Xm,
-                                          const double2* X0, const double2* Xp, const double2* Ym,
-                                          const double2* Y0, const double2* Yp, const double2* Zm,
-                                          const double2* Z0, Edge3& E) {
+                                          double ihzm, double hdz, const V* Xm, const V* X0, const V* Xp,
+                                          const V* Ym, const V* Y0, const V* Yp, const V* Zm, const V* Z0,
+                                          Edge3<V>& E) {
   E.f[0] = C.in_ij && free_x(g, C.i, C.j, k);
   E.f[1] = C.in_ij && free_y(g, C.i, C.j, k);
   E.f[2] = C.in_ij && k >= 0 && free_z(g, C.i, C.j, k);
 #define T_(P, di, dj) P[c0 + (dj) * PITCH + (di)]
-  const double2 x00 = T_(X0, 0, 0), y00 = T_(Y0, 0, 0), z00 = T_(Z0, 0, 0);
+  const V x00 = T_(X0, 0, 0), y00 = T_(Y0, 0, 0), z00 = T_(Z0, 0, 0);
   // face weights W = hdual / (mu0 A)
   const double wz = hdz * C.pxy, wz_y = hdz * C.pxym, wz_x = hdz * C.pxmy;      // Fz(m), Fz(m-ey), Fz(m-ex)
   const double wy = C.cyx * ihz, wy_z = C.cyx * ihzm, wy_x = C.cyxm * ihz;      // Fy(m), Fy(m-ez), Fy(m-ex)
@@ -300,10 +302,10 @@ __device__ __forceinline__ void stencil3p(const Grid& g, const Column& C, int c0
   // G = W * circulation (right-hand rule about the face normal), accumulated
   // into (K v)_x = Gz - Gz(m-ey) - Gy + Gy(m-ez), (K v)_y = Gx - Gx(m-ez) - Gz + Gz(m-ex),
   // (K v)_z = Gy - Gy(m-ex) - Gx + Gx(m-ey) face by face (short live ranges)
-  double2 qx, qy, qz, G;
+  V qx, qy, qz, G;
   G = cscale(wz, csub(cadd(x00, T_(Y0, 1, 0)), cadd(T_(X0, 0, 1), y00)));          // Fz(m)
   qx = G;
-  qy = make_double2(-G.x, -G.y);
+  qy = cscale(-1.0, G);
   G = cscale(wy, csub(cadd(z00, T_(Xp, 0, 0)), cadd(T_(Z0, 1, 0), x00)));          // Fy(m)
   qx = csub(qx, G);
   qz = G;
@@ -334,12 +336,10 @@ __device__ __forceinline__ void stencil3p(const Grid& g, const Column& C, int c0
   E.p[2] = z00;
 }
 
-template <int TYV>
+template <int TYV, typename V>
 __device__ __forceinline__ void stencil3(const Grid& g, const Column& C, int k, double ihz, double ihzm,
-                                         double hdz, const double2* Xm, const double2* X0,
-                                         const double2* Xp, const double2* Ym, const double2* Y0,
-                                         const double2* Yp, const double2* Zm, const double2* Z0,
-                                         Edge3& E) {
+                                         double hdz, const V* Xm, const V* X0, const V* Xp, const V* Ym,
+                                         const V* Y0, const V* Yp, const V* Zm, const V* Z0, Edge3<V>& E) {
   stencil3p<Tile<TYV>::HX>(g, C, C.c0, k, ihz, ihzm, hdz, Xm, X0, Xp, Ym, Y0, Yp, Zm, Z0, E);
 }
 
@@ -347,30 +347,19 @@ __device__ __forceinline__ void stencil3(const Grid& g, const Column& C, int k, 
 // (K = T^T W T, §2.2: v^T K v = sum_f W_f C_f(v)^2 over all faces,
 // unconjugated square for the complex-symmetric form).  Summed over all
 // nodes every face is counted once; it reads only the +x, +y, +z neighbours.
-__device__ __forceinline__ double2 csq(double2 a) { return make_double2(fma(a.x, a.x, -a.y * a.y), 2.0 * a.x * a.y); }
-
-template <int TYV>
-__device__ __forceinline__ double2 faces_quad(const Column& C, double ihz, double hdz, const double2* X0,
-                                              const double2* Xp, const double2* Y0, const double2* Yp,
-                                              const double2* Z0) {
+template <int TYV, typename V>
+__device__ __forceinline__ V faces_quad(const Column& C, double ihz, double hdz, const V* X0, const V* Xp,
+                                        const V* Y0, const V* Yp, const V* Z0) {
   constexpr int HX = Tile<TYV>::HX;
   const int c0 = C.c0;
-  const double2 x00 = X0[c0], y00 = Y0[c0], z00 = Z0[c0];
-  const double2 Fz = csub(cadd(x00, Y0[c0 + 1]), cadd(X0[c0 + HX], y00));
-  const double2 Fy = csub(cadd(z00, Xp[c0]), cadd(Z0[c0 + 1], x00));
-  const double2 Fx = csub(cadd(y00, Z0[c0 + HX]), cadd(Yp[c0], z00));
-  double2 acc = cscale(hdz * C.pxy, csq(Fz));
+  const V x00 = X0[c0], y00 = Y0[c0], z00 = Z0[c0];
+  const V Fz = csub(cadd(x00, Y0[c0 + 1]), cadd(X0[c0 + HX], y00));
+  const V Fy = csub(cadd(z00, Xp[c0]), cadd(Z0[c0 + 1], x00));
+  const V Fx = csub(cadd(y00, Z0[c0 + HX]), cadd(Yp[c0], z00));
+  V acc = cscale(hdz * C.pxy, csq(Fz));
   acc = cadd(acc, cscale(C.cyx * ihz, csq(Fy)));
   return cadd(acc, cscale(C.cxy * ihz, csq(Fx)));
 }
-
-// ---------------------------------------------------------------- pass 2
-// k_delta: z^T K z of the split solver, per shift, from the node's own faces
-// (faces_quad); the mass term s z^T M z is pointwise and comes with pass 1
-// (k_init for z_0).  It reads z once (16 B per unknown per
-// shift) with a +1 halo; plane sets q = {X(q), Y(q), Z(q)} in a 4-deep ring
-// (step k reads sets k and k+1, sets k+2 and k+3 in flight): 12 tiles, 66 KB,
-// three CTAs per SM.
 
 // Split solver finalisation (last CTA of pass 2): per-shift sums of the pass-1
 // partials (gamma, eps, mu, ||r||^2) and the pass-2 partial delta, then
@@ -413,7 +402,7 @@ __device__ void finalize_split(const SweepArgs& A) {
     }
     sq.iters += 1;
     sq.relres = sqrt(v[6]) / sq.fnorm;
-    if (sq.relres <= A.ctl->tol) {
+    if (sq.relres <= sq.tol) {
       sq.active = 0;
       sq.status = 1;
     } else if ((gam.x == 0.0 && gam.y == 0.0) || (sq.rho.x == 0.0 && sq.rho.y == 0.0)) {
@@ -479,7 +468,7 @@ __device__ void finalize(const SweepArgs& A) {
       } else {
         sq.iters += 1;
         sq.relres = sqrt(cr) / sq.fnorm;
-        if (sq.relres <= A.ctl->tol) {
+        if (sq.relres <= sq.tol) {
           sq.active = 0;
           sq.status = 1;
         } else if ((sq.rho.x == 0.0 && sq.rho.y == 0.0) || (sum.x == 0.0 && sum.y == 0.0)) {
@@ -540,44 +529,284 @@ __device__ __forceinline__ void block_coords(const SweepArgs& A, int& a, int& tx
   pidx = a * (A.nzc * ntx * nty) + (zc * nty + ty) * ntx + tx;
 }
 
+// ---------------------------------------------------------------- layouts
+// Shift s's vectors in a shift block: complex -> [3][Nn] double2 at
+// s * 3 Nn (include/tem_b200.h); real -> [3][NnP] double at the start of the
+// same region (Grid::px, NnP).
+template <typename V>
+__device__ __forceinline__ V* vbase(const double2* p, int s, const Grid& g) {
+  if constexpr (VT<V>::kReal)
+    return reinterpret_cast<V*>(const_cast<double2*>(p)) + (long long)s * 6 * g.Nn;
+  else
+    return const_cast<double2*>(p) + (long long)s * 3 * g.Nn;
+}
+template <typename V>
+__device__ __forceinline__ long long vcomp(const Grid& g) {
+  if constexpr (VT<V>::kReal) return g.NnP; else return g.Nn;
+}
+template <typename V>
+__device__ __forceinline__ int vrow(const Grid& g) {
+  if constexpr (VT<V>::kReal) return g.px; else return g.n[0] + 1;
+}
+
 // ---------------------------------------------------------------- sweeps
-// One kernel for the three modes.  Plane sets q = {X(q+1), Y(q+1), Z(q)} of
-// the swept vector v live in a ring: X,Y slots q mod 5, Z slots q mod 4,
+// One kernel for all modes.  Plane sets q = {X(q+1), Y(q+1), Z(q)} of the
+// swept vector v live in a ring: X,Y slots q mod 5, Z slots q mod 4,
 // mbarrier q mod 5.  MODE 0/2: v is read as is, three sets run ahead of the
-// arithmetic.  MODE 1: v = p_old is loaded into the ring and z into a 2-slot
+// arithmetic.  MODE 1/3/4: v = p_old is loaded into the ring and z into a
 // staging area; when set q has landed it is combined IN PLACE into
-// p_new = z + beta p_old (at the end of step q-1, two sets ahead), so MODE 1
-// needs 20 tiles (110 KB at TY = 8) and also runs 2 CTAs per SM.
-template <int MODE, int TYV = (MODE >= 3 ? kTYSplit : kTYTwoSweep)>
-__global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
-    k_sweep(const __grid_constant__ SweepArgs A, const __grid_constant__ CUtensorMap tmv,
-            const __grid_constant__ CUtensorMap tmz) {
+// p_new = z + beta p_old (at the end of step q-1, two sets ahead).
+// The split modes run a real shift (ShiftState::real) in real arithmetic:
+// the same body over V = double, half-size tiles in the same ring slots.
+struct Partials {
+  double2 c, e, m, q;
+  double r;
+};
+
+template <int MODE, int TYV, typename V>
+__device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap* tmv, const CUtensorMap* tmz,
+                                           int s, int tx0, int ty0, int kb, int ke, double2 sh2, double2 alpha2,
+                                           double2 beta2, double2 alpha_prev2, double2* ring2, uint64_t* bar,
+                                           double* zih, double* zhd, Partials& P) {
   TEM_TILE_CONSTANTS(TYV);
   constexpr bool kZ = (MODE == 1 || MODE == 3 || MODE == 4);   // p_new = z + beta p_old formed in smem
   constexpr bool kUpd = (MODE == 3 || MODE == 4);               // split pass 1: full update
-  extern __shared__ unsigned char smem_raw[];
-  double2* ring = smem_align128(smem_raw);
-  double2* rX = ring;                        // [R_XY] slots
-  double2* rY = ring + R_XY * TS2;           // [R_XY]
-  double2* rZ = ring + 2 * R_XY * TS2;       // [R_Z]
+  constexpr int kW = sizeof(V) / 8;                             // doubles per value
+  constexpr int TSV = TS2 * 2 / kW;                             // slot pitch in V
+  constexpr int TILE_V = HX * HY * (int)sizeof(V);              // bytes of one TMA plane tile
+  V* ring = reinterpret_cast<V*>(ring2);
+  V* rX = ring;                        // [R_XY] slots
+  V* rY = ring + R_XY * TSV;           // [R_XY]
+  V* rZ = ring + 2 * R_XY * TSV;       // [R_Z]
   // z staging [RS][3 tiles]: 2 sets (MODE 1, 4); 4 sets (MODE 3), so that the
   // node's own z_i (X, Y of set k-1, Z of set k) is still staged at step k
   constexpr bool kZOwn = (MODE == 3);   // own z_i from staging (MODE 4: re-read, fewer registers)
   constexpr int RS = kZOwn ? 4 : 2;
-  double2* zs = ring + (2 * R_XY + R_Z) * TS2;
+  V* zs = ring + (2 * R_XY + R_Z) * TSV;
+  const Grid& g = A.g;
+  const int tid = threadIdx.x;
+  const V sh = VT<V>::from(sh2), alpha = VT<V>::from(alpha2), beta = VT<V>::from(beta2);
+  const V alpha_prev = VT<V>::from(alpha_prev2);
+  V acc_c = VT<V>::zero(), acc_e = VT<V>::zero(), acc_m = VT<V>::zero(), acc_q = VT<V>::zero();
+  double acc_r = 0.0;
+  // MODE 4: x_{i+1} = x_{i-1} + (alpha_i + a/beta_i) p_i - (a/beta_i) z_i, a = alpha_{i-1}
+  // (exact rewrite of alpha_{i-1} p_{i-1} + alpha_i p_i).  Its rounding error,
+  // relative to the x increment, grows like |z_i| / |beta_i p_{i-1}|; when
+  // |beta_i| < 1/32 (about 2% of iterations) p_{i-1} is re-read instead (x_direct).
+  const bool x_direct = MODE == 4 && (A.force_xdirect || cabs2(beta) < 1.0 / 1024.0);
+  // x_{i+1} = x_{i-1} + xc_p p_i + xc_z (z_i, or p_{i-1} when x_direct)
+  V xc_p = alpha, xc_z = alpha_prev;
+  if (MODE == 4 && !x_direct) {
+    xc_z = cdiv(alpha_prev, beta);
+    xc_p = cadd(alpha, xc_z);
+    xc_z = cscale(-1.0, xc_z);
+  }
+
+  const Column C = make_column<TYV>(g, tx0, ty0);
+  const long long cst = vcomp<V>(g);                 // component stride of this layout
+  const int rowp = vrow<V>(g);                       // node row pitch of this layout
+  const int nx1 = g.n[0] + 1, ny1 = g.n[1] + 1;
+  V* out = vbase<V>(A.out, s, g);
+  V* xv = vbase<V>(A.x, s, g);
+  V* zv = vbase<V>(A.z, s, g);
+  const V* zin = vbase<V>(A.zin, s, g);
+  const V* pold = vbase<V>(A.pold, s, g);
+  for (int q = tid; q <= ke - kb; q += NT) {
+    const int k = kb - 1 + q;
+    zih[q] = k >= 0 ? __ldg(g.ih[2] + k) : 0.0;
+    if (q < ke - kb) zhd[q] = __ldg(g.hdm[2] + kb + q);
+  }
+  // Set kb-2 carries no Z tile: Z(kb-2) is never read, and with five sets in
+  // flight its Z slot is the one set kb+2 fills (two TMAs into one slot race).
+  auto issue = [&](int q) {
+    const int sx = pmod(q, R_XY), sz = pmod(q, R_Z);
+    const bool with_z = q > kb - 2;
+    const int ntile = (with_z ? 3 : 2) * (kZ ? 2 : 1);
+    mbar_expect_tx(&bar[sx], ntile * TILE_V);
+    const int cx = kW * (tx0 - 1), cy = ty0 - 1;
+    tma_tile(rX + sx * TSV, tmv, cx, cy, q + 1, 0, s, &bar[sx]);
+    tma_tile(rY + sx * TSV, tmv, cx, cy, q + 1, 1, s, &bar[sx]);
+    if (with_z) tma_tile(rZ + sz * TSV, tmv, cx, cy, q, 2, s, &bar[sx]);
+    if (kZ) {
+      V* d = zs + pmod(q, RS) * 3 * TSV;
+      tma_tile(d, tmz, cx, cy, q + 1, 0, s, &bar[sx]);
+      tma_tile(d + TSV, tmz, cx, cy, q + 1, 1, s, &bar[sx]);
+      if (with_z) tma_tile(d + 2 * TSV, tmz, cx, cy, q, 2, s, &bar[sx]);
+    }
+  };
+  uint32_t phase = 0;   // bit b = parity of the next wait on bar[b]
+  auto wait_set = [&](int q) {
+    const int b = pmod(q, R_XY);
+    mbar_wait(&bar[b], (phase >> b) & 1u);
+    phase ^= 1u << b;
+  };
+  // MODE 1/3/4: wait for set q and form p_new = z + beta p_old in its ring slots
+  auto combine = [&](int q) {
+    wait_set(q);
+    const V* d = zs + pmod(q, RS) * 3 * TSV;
+    V* dX = rX + pmod(q, R_XY) * TSV;
+    V* dY = rY + pmod(q, R_XY) * TSV;
+    V* dZ = rZ + pmod(q, R_Z) * TSV;
+    const bool with_z = q > kb - 2;
+    for (int e = tid; e < HX * HY; e += NT) {
+      dX[e] = cfma(beta, dX[e], d[e]);
+      dY[e] = cfma(beta, dY[e], d[TSV + e]);
+      if (with_z) dZ[e] = cfma(beta, dZ[e], d[2 * TSV + e]);
+    }
+  };
+  if (tid == 0) {
+    for (int q = 0; q < R_XY; ++q) mbar_init(&bar[q], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (!kZ) {
+    if (tid == 0)
+      for (int q = kb - 2; q <= min(kb + 2, ke - 1); ++q) issue(q);
+    wait_set(kb - 2);
+    wait_set(kb - 1);
+  } else {
+    // z staging has 2 slots: sets enter two at a time
+    if (tid == 0) {
+      issue(kb - 2);
+      issue(kb - 1);
+    }
+    for (int q = kb - 2; q <= kb; ++q) {
+      combine(q);
+      __syncthreads();
+      if (tid == 0 && q + 2 <= ke - 1) {
+        fence_proxy_async();
+        issue(q + 2);
+      }
+    }
+  }
+
+  // centre operands (mass; MODE 2: x, z; MODE 4: x, z) of the next step, loaded a step ahead
+  double mN[3];
+  V xN[3], zN[3];
+  auto load_centre = [&](int k) {
+    const long long node = ((long long)k * ny1 + C.j) * nx1 + C.i;
+    const long long nodeV = ((long long)k * ny1 + C.j) * rowp + C.i;
+    const bool ok = C.in_ij && k < g.n[2];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      mN[c] = ok ? __ldg(A.mass + c * g.Nn + node) : 0.0;
+      const long long slot = c * cst + nodeV;
+      if (MODE == 2) {
+        xN[c] = ok ? xv[slot] : VT<V>::zero();
+        zN[c] = ok ? zv[slot] : VT<V>::zero();
+      }
+      if (MODE == 4) {
+        xN[c] = ok ? xv[slot] : VT<V>::zero();
+        zN[c] = ok ? __ldcg(zin + slot) : VT<V>::zero();
+      }
+    }
+  };
+  load_centre(kb);
+
+  // ring slots of the planes the stencil reads: X, Y of k-1, k, k+1 (sets
+  // k-2, k-1, k), Z of k-1, k (sets k-1, k); rotated once per step
+  int sxm = pmod(kb - 2, R_XY), sx0 = pmod(kb - 1, R_XY), sxp = pmod(kb, R_XY);
+  int szm = pmod(kb - 1, R_Z), sz0 = pmod(kb, R_Z);
+  const long long col = (long long)C.j * rowp + C.i;   // own column, component 0, plane 0
+  const long long plane = (long long)rowp * ny1;
+#pragma unroll 1
+  for (int k = kb; k < ke; ++k) {
+    if (!kZ) wait_set(k);
+    Edge3<V> E;
+    stencil3<TYV>(g, C, k, zih[k - kb + 1], zih[k - kb], zhd[k - kb], rX + sxm * TSV, rX + sx0 * TSV,
+                  rX + sxp * TSV, rY + sxm * TSV, rY + sx0 * TSV, rY + sxp * TSV, rZ + szm * TSV,
+                  rZ + sz0 * TSV, E);
+    sxm = sx0;
+    sx0 = sxp;
+    sxp = sxp + 1 == R_XY ? 0 : sxp + 1;
+    szm = sz0;
+    sz0 = sz0 + 1 == R_Z ? 0 : sz0 + 1;
+    const long long ek = col + (long long)k * plane;
+    if (kZOwn) {   // own z_i from the staging tiles: X, Y of set k-1, Z of set k
+      const V* zk1 = zs + pmod(k - 1, RS) * 3 * TSV;
+      const V* zk = zs + pmod(k, RS) * 3 * TSV;
+      zN[0] = zk1[C.c0];
+      zN[1] = zk1[TSV + C.c0];
+      zN[2] = zk[2 * TSV + C.c0];
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      if (!E.f[c]) continue;
+      const long long e = ek + c * cst;
+      const V q = cfma(sh, cscale(mN[c], E.p[c]), E.q[c]);   // (K + s M) v
+      if (kUpd) {
+        const V D = VT<V>::make(E.kd[c] + mN[c] * sh2.x, mN[c] * sh2.y);
+        double nD;                                                      // |D|^2
+        const V zn = csub(zN[c], cmul(alpha, cmul(q, crcp(D, nD))));   // z_i - alpha D^-1 A p_i
+        st_stream(out + e, E.p[c]);                                     // p_i
+        st_stream(zv + e, zn);                                          // z_{i+1}
+        if (MODE == 4) {   // x_{i+1} = x_{i-1} + alpha_{i-1} p_{i-1} + alpha_i p_i
+          if (x_direct)
+            st_stream(xv + e, cfma(xc_p, E.p[c], cfma(xc_z, __ldcg(pold + e), xN[c])));
+          else   // p_{i-1} = (p_i - z_i) / beta_i: no re-read of p_{i-1}
+            st_stream(xv + e, cfma(xc_z, zN[c], cfma(xc_p, E.p[c], xN[c])));
+        }
+        const V zq = csq(zn);                                           // z_{i+1}^2
+        acc_c = cfma(D, zq, acc_c);                  // gamma_{i+1} = (D z)^T z
+        acc_r = fma(nD, cabs2(zn), acc_r);           // ||D z||^2
+        acc_q = sfma(mN[c], zq, acc_q);              // z^T M z
+        acc_e = cfma(zn, q, acc_e);                  // z_{i+1}^T A p_i
+        acc_m = cfma(E.p[c], q, acc_m);              // p_i^T A p_i
+      } else if (MODE == 0) {
+        out[e] = q;
+      } else if (MODE == 1) {
+        st_stream(out + e, E.p[c]);      // p_new
+        acc_c = cfma(E.p[c], q, acc_c);  // p^T A p
+      } else {
+        const V D = VT<V>::make(E.kd[c] + mN[c] * sh2.x, mN[c] * sh2.y);
+        st_stream(xv + e, cfma(alpha, E.p[c], xN[c]));
+        const V zn = csub(zN[c], cmul(alpha, cdiv(q, D)));   // z - alpha D^-1 q
+        st_stream(zv + e, zn);
+        const V rn = cmul(D, zn);                           // r = D z
+        acc_c = cfma(rn, zn, acc_c);
+        acc_r += cabs2(rn);
+      }
+    }
+    // centre operands of step k+1: issued now, consumed after step k+1's stencil
+    if (k + 1 < ke) load_centre(k + 1);
+    // MODE 1/3/4: set k+1's ring slots held set k-4/k-3 (no longer read): combine it now
+    if (kZ && k + 1 <= ke - 1) combine(k + 1);
+    __syncthreads();   // all reads of set k-2 done -> its slots may be refilled
+    if (tid == 0 && k + 3 <= ke - 1) {
+      fence_proxy_async();
+      issue(k + 3);
+    }
+  }
+  P.c = VT<V>::cplx(acc_c);
+  P.e = VT<V>::cplx(acc_e);
+  P.m = VT<V>::cplx(acc_m);
+  P.q = VT<V>::cplx(acc_q);
+  P.r = acc_r;
+}
+
+// tmv/tmz: tensor maps of the swept vector and of z over complex shift
+// blocks; tmvr/tmzr: the same buffers in the real layout (split modes).
+template <int MODE, int TYV = (MODE >= 3 ? kTYSplit : kTYTwoSweep)>
+__global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
+    k_sweep(const __grid_constant__ SweepArgs A, const __grid_constant__ CUtensorMap tmv,
+            const __grid_constant__ CUtensorMap tmz, const __grid_constant__ CUtensorMap tmvr,
+            const __grid_constant__ CUtensorMap tmzr) {
+  constexpr int NT = Tile<TYV>::NT;
+  constexpr bool kUpd = (MODE == 3 || MODE == 4);
+  extern __shared__ unsigned char smem_raw[];
+  double2* ring = smem_align128(smem_raw);
   __shared__ __align__(8) uint64_t bar[R_XY];
   __shared__ double red[3 * NT / 32];
   __shared__ double zih[kMaxChunk + 1];     // ih_z[k] for k = kb-1 .. ke-1
   __shared__ double zhd[kMaxChunk];         // hdual_z[k]/mu0 for k = kb .. ke-1
 
-  const Grid& g = A.g;
   int a, tx0, ty0, kb, ke;
   int pidx;
   block_coords<TYV>(A, a, tx0, ty0, kb, ke, pidx);
   const int tid = threadIdx.x;
 
   double2 sh = czero(), alpha = czero(), beta = czero(), alpha_prev = czero();
-  bool live;
+  bool live, real = false;
   int s = a;
   if (MODE == 0) {
     sh = A.shifts[s];
@@ -592,199 +821,28 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
       beta = st.beta;
       alpha_prev = st.alpha_prev;
       live = st.active != 0;
+      real = kUpd && st.real;
     }
   }
-  double2 acc_c = czero(), acc_e = czero(), acc_m = czero(), acc_q = czero();
-  double acc_r = 0.0;
-  // MODE 4: x_{i+1} = x_{i-1} + (alpha_i + a/beta_i) p_i - (a/beta_i) z_i, a = alpha_{i-1}
-  // (exact rewrite of alpha_{i-1} p_{i-1} + alpha_i p_i).  Its rounding error,
-  // relative to the x increment, grows like |z_i| / |beta_i p_{i-1}|; when
-  // |beta_i| < 1/32 (about 2% of iterations) p_{i-1} is re-read instead (x_direct).
-  const bool x_direct = MODE == 4 && (A.force_xdirect || beta.x * beta.x + beta.y * beta.y < 1.0 / 1024.0);
-  // x_{i+1} = x_{i-1} + xc_p p_i + xc_z (z_i, or p_{i-1} when x_direct)
-  double2 xc_p = alpha, xc_z = alpha_prev;
-  if (MODE == 4 && !x_direct) {
-    xc_z = cdiv(alpha_prev, beta);
-    xc_p = cadd(alpha, xc_z);
-    xc_z = make_double2(-xc_z.x, -xc_z.y);
-  }
-
+  Partials P{};
   if (live) {
-    const Column C = make_column<TYV>(g, tx0, ty0);
-    const long long vs = (long long)s * 3 * g.Nn;
-    const int nx1 = g.n[0] + 1, ny1 = g.n[1] + 1;
-    for (int q = tid; q <= ke - kb; q += NT) {
-      const int k = kb - 1 + q;
-      zih[q] = k >= 0 ? __ldg(g.ih[2] + k) : 0.0;
-      if (q < ke - kb) zhd[q] = __ldg(g.hdm[2] + kb + q);
-    }
-    // Set kb-2 carries no Z tile: Z(kb-2) is never read, and with five sets in
-    // flight its Z slot is the one set kb+2 fills (two TMAs into one slot race).
-    auto issue = [&](int q) {
-      const int sx = pmod(q, R_XY), sz = pmod(q, R_Z);
-      const bool with_z = q > kb - 2;
-      const int ntile = (with_z ? 3 : 2) * (kZ ? 2 : 1);
-      mbar_expect_tx(&bar[sx], ntile * TILE_BYTES);
-      const int cx = 2 * (tx0 - 1), cy = ty0 - 1;
-      tma_tile(rX + sx * TS2, &tmv, cx, cy, q + 1, 0, s, &bar[sx]);
-      tma_tile(rY + sx * TS2, &tmv, cx, cy, q + 1, 1, s, &bar[sx]);
-      if (with_z) tma_tile(rZ + sz * TS2, &tmv, cx, cy, q, 2, s, &bar[sx]);
-      if (kZ) {
-        double2* d = zs + pmod(q, RS) * 3 * TS2;
-        tma_tile(d, &tmz, cx, cy, q + 1, 0, s, &bar[sx]);
-        tma_tile(d + TS2, &tmz, cx, cy, q + 1, 1, s, &bar[sx]);
-        if (with_z) tma_tile(d + 2 * TS2, &tmz, cx, cy, q, 2, s, &bar[sx]);
-      }
-    };
-    uint32_t phase = 0;   // bit b = parity of the next wait on bar[b]
-    auto wait_set = [&](int q) {
-      const int b = pmod(q, R_XY);
-      mbar_wait(&bar[b], (phase >> b) & 1u);
-      phase ^= 1u << b;
-    };
-    // MODE 1: wait for set q and form p_new = z + beta p_old in its ring slots
-    auto combine = [&](int q) {
-      wait_set(q);
-      const double2* d = zs + pmod(q, RS) * 3 * TS2;
-      double2* dX = rX + pmod(q, R_XY) * TS2;
-      double2* dY = rY + pmod(q, R_XY) * TS2;
-      double2* dZ = rZ + pmod(q, R_Z) * TS2;
-      const bool with_z = q > kb - 2;
-      for (int e = tid; e < HX * HY; e += NT) {
-        dX[e] = cfma(beta, dX[e], d[e]);
-        dY[e] = cfma(beta, dY[e], d[TS2 + e]);
-        if (with_z) dZ[e] = cfma(beta, dZ[e], d[2 * TS2 + e]);
-      }
-    };
-    if (tid == 0) {
-      for (int q = 0; q < R_XY; ++q) mbar_init(&bar[q], 1);
-      fence_barrier_init();
-    }
-    __syncthreads();
-    if (!kZ) {
-      if (tid == 0)
-        for (int q = kb - 2; q <= min(kb + 2, ke - 1); ++q) issue(q);
-      wait_set(kb - 2);
-      wait_set(kb - 1);
+    if constexpr (kUpd) {
+      if (real)
+        sweep_body<MODE, TYV, double>(A, &tmvr, &tmzr, s, tx0, ty0, kb, ke, sh, alpha, beta, alpha_prev,
+                                      ring, bar, zih, zhd, P);
+      else
+        sweep_body<MODE, TYV, double2>(A, &tmv, &tmz, s, tx0, ty0, kb, ke, sh, alpha, beta, alpha_prev,
+                                       ring, bar, zih, zhd, P);
     } else {
-      // z staging has 2 slots: sets enter two at a time
-      if (tid == 0) {
-        issue(kb - 2);
-        issue(kb - 1);
-      }
-      for (int q = kb - 2; q <= kb; ++q) {
-        combine(q);
-        __syncthreads();
-        if (tid == 0 && q + 2 <= ke - 1) {
-          fence_proxy_async();
-          issue(q + 2);
-        }
-      }
-    }
-
-    // centre operands (mass; MODE 2: x, z; MODE 4: x, z) of the next step, loaded a step ahead
-    auto node_of = [&](int k) { return ((long long)k * ny1 + C.j) * nx1 + C.i; };
-    double mN[3];
-    double2 xN[3], zN[3];
-    auto load_centre = [&](int k) {
-      const long long node = node_of(k);
-      const bool ok = C.in_ij && k < g.n[2];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const long long slot = (long long)c * g.Nn + node;
-        mN[c] = ok ? __ldg(A.mass + slot) : 0.0;
-        if (MODE == 2) {
-          xN[c] = ok ? A.x[vs + slot] : czero();
-          zN[c] = ok ? A.z[vs + slot] : czero();
-        }
-        if (MODE == 4) {
-          xN[c] = ok ? A.x[vs + slot] : czero();
-          zN[c] = ok ? __ldcg(A.zin + vs + slot) : czero();
-        }
-      }
-    };
-    load_centre(kb);
-
-    // ring slots of the planes the stencil reads: X, Y of k-1, k, k+1 (sets
-    // k-2, k-1, k), Z of k-1, k (sets k-1, k); rotated once per step
-    int sxm = pmod(kb - 2, R_XY), sx0 = pmod(kb - 1, R_XY), sxp = pmod(kb, R_XY);
-    int szm = pmod(kb - 1, R_Z), sz0 = pmod(kb, R_Z);
-    const long long col = vs + (long long)C.j * nx1 + C.i;   // own column, component 0, plane 0
-    const long long plane = (long long)nx1 * ny1;
-#pragma unroll 1
-    for (int k = kb; k < ke; ++k) {
-      if (!kZ) wait_set(k);
-      Edge3 E;
-      stencil3<TYV>(g, C, k, zih[k - kb + 1], zih[k - kb], zhd[k - kb], rX + sxm * TS2, rX + sx0 * TS2,
-               rX + sxp * TS2, rY + sxm * TS2, rY + sx0 * TS2, rY + sxp * TS2, rZ + szm * TS2,
-               rZ + sz0 * TS2, E);
-      sxm = sx0;
-      sx0 = sxp;
-      sxp = sxp + 1 == R_XY ? 0 : sxp + 1;
-      szm = sz0;
-      sz0 = sz0 + 1 == R_Z ? 0 : sz0 + 1;
-      const long long ek = col + (long long)k * plane;
-      if (kZOwn) {   // own z_i from the staging tiles: X, Y of set k-1, Z of set k
-        const double2* zk1 = zs + pmod(k - 1, RS) * 3 * TS2;
-        const double2* zk = zs + pmod(k, RS) * 3 * TS2;
-        zN[0] = zk1[C.c0];
-        zN[1] = zk1[TS2 + C.c0];
-        zN[2] = zk[2 * TS2 + C.c0];
-      }
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        if (!E.f[c]) continue;
-        const long long e = ek + (long long)c * g.Nn;
-        const double2 q = cfma(sh, cscale(mN[c], E.p[c]), E.q[c]);   // (K + s M) v
-        if (kUpd) {
-          const double2 D = make_double2(E.kd[c] + mN[c] * sh.x, mN[c] * sh.y);
-          double nD;                                                      // |D|^2
-          const double2 zn = csub(zN[c], cmul(alpha, cmul(q, crcp(D, nD))));   // z_i - alpha D^-1 A p_i
-          st_stream(A.out + e, E.p[c]);                                   // p_i
-          st_stream(A.z + e, zn);                                         // z_{i+1}
-          if (MODE == 4) {   // x_{i+1} = x_{i-1} + alpha_{i-1} p_{i-1} + alpha_i p_i
-            if (x_direct)
-              st_stream(A.x + e, cfma(xc_p, E.p[c], cfma(xc_z, __ldcg(A.pold + e), xN[c])));
-            else   // p_{i-1} = (p_i - z_i) / beta_i: no re-read of p_{i-1}
-              st_stream(A.x + e, cfma(xc_z, zN[c], cfma(xc_p, E.p[c], xN[c])));
-          }
-          const double2 zq = csq(zn);                                     // z_{i+1}^2
-          acc_c = cfma(D, zq, acc_c);                  // gamma_{i+1} = (D z)^T z
-          acc_r = fma(nD, fma(zn.x, zn.x, zn.y * zn.y), acc_r);            // ||D z||^2
-          acc_q = make_double2(fma(mN[c], zq.x, acc_q.x), fma(mN[c], zq.y, acc_q.y));   // z^T M z
-          acc_e = cfma(zn, q, acc_e);                                     // z_{i+1}^T A p_i
-          acc_m = cfma(E.p[c], q, acc_m);                                 // p_i^T A p_i
-        } else if (MODE == 0) {
-          A.out[e] = q;
-        } else if (MODE == 1) {
-          st_stream(A.out + e, E.p[c]);      // p_new
-          acc_c = cfma(E.p[c], q, acc_c);    // p^T A p
-        } else {
-          const double2 D = make_double2(E.kd[c] + mN[c] * sh.x, mN[c] * sh.y);
-          st_stream(A.x + e, cfma(alpha, E.p[c], xN[c]));
-          const double2 zn = csub(zN[c], cmul(alpha, cdiv(q, D)));   // z - alpha D^-1 q
-          st_stream(A.z + e, zn);
-          const double2 rn = cmul(D, zn);                           // r = D z
-          acc_c = cfma(rn, zn, acc_c);
-          acc_r += rn.x * rn.x + rn.y * rn.y;
-        }
-      }
-      // centre operands of step k+1: issued now, consumed after step k+1's stencil
-      if (k + 1 < ke) load_centre(k + 1);
-      // MODE 1: set k+1's ring slots held set k-4/k-3 (no longer read): combine it now
-      if (kZ && k + 1 <= ke - 1) combine(k + 1);
-      __syncthreads();   // all reads of set k-2 done -> its slots may be refilled
-      if (tid == 0 && k + 3 <= ke - 1) {
-        fence_proxy_async();
-        issue(k + 3);
-      }
+      sweep_body<MODE, TYV, double2>(A, &tmv, &tmz, s, tx0, ty0, kb, ke, sh, alpha, beta, alpha_prev, ring,
+                                     bar, zih, zhd, P);
     }
   }
   if (MODE == 0) return;
   if (kUpd) {
     __shared__ double red9[kSplitPart * NT / 32];
-    const double2 dm = cmul(sh, acc_q);   // s z^T M z
-    double v[kSplitPart] = {acc_c.x, acc_c.y, acc_e.x, acc_e.y, acc_m.x, acc_m.y, acc_r, 0.0, 0.0, dm.x, dm.y};
+    const double2 dm = cmul(sh, P.q);   // s z^T M z
+    double v[kSplitPart] = {P.c.x, P.c.y, P.e.x, P.e.y, P.m.x, P.m.y, P.r, 0.0, 0.0, dm.x, dm.y};
 #pragma unroll
     for (int t = 0; t < kSplitPart; ++t)
       if (t < 7 || t > 8)
@@ -801,6 +859,8 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
     }
     return;
   }
+  double2 acc_c = P.c;
+  double acc_r = P.r;
   block_sum_n<NT>(acc_c, acc_r, red);
   if (tid == 0) {
     A.part_c[pidx] = acc_c;
@@ -810,14 +870,71 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
   finalize<MODE, TYV>(A);
 }
 
-}  // namespace tem
-
-namespace tem {
+// ---------------------------------------------------------------- pass 2
+// k_delta: z^T K z of the split solver, per shift, from the node's own faces
+// (faces_quad); the mass term s z^T M z is pointwise and comes with pass 1
+// (k_init for z_0).  It reads z once (16 B per unknown per shift; 8 B for a
+// real shift) with a +1 halo; plane sets q = {X(q), Y(q), Z(q)} in a 4-deep
+// ring (step k reads sets k and k+1, sets k+2 and k+3 in flight): 12 tiles,
+// 90 KB at TY = 12, two CTAs per SM.
+template <int TYV, typename V>
+__device__ __forceinline__ double2 delta_body(const SweepArgs& A, const CUtensorMap* tmv, int s, int tx0,
+                                              int ty0, int kb, int ke, double2* ring2, uint64_t* bar,
+                                              double* zih, double* zhd) {
+  TEM_TILE_CONSTANTS(TYV);
+  constexpr int kW = sizeof(V) / 8;
+  constexpr int TSV = TS2 * 2 / kW;
+  constexpr int TILE_V = HX * HY * (int)sizeof(V);
+  V* ring = reinterpret_cast<V*>(ring2);
+  const Grid& g = A.g;
+  const int tid = threadIdx.x;
+  V acc = VT<V>::zero();
+  const Column C = make_column<TYV>(g, tx0, ty0);
+  for (int q = tid; q < ke - kb; q += NT) {
+    zih[q] = __ldg(g.ih[2] + kb + q);
+    zhd[q] = __ldg(g.hdm[2] + kb + q);
+  }
+  auto issue = [&](int q) {
+    const int b = q % R_D;
+    mbar_expect_tx(&bar[b], 3 * TILE_V);
+    const int cx = kW * (tx0 - 1), cy = ty0 - 1;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) tma_tile(ring + (b * 3 + c) * TSV, tmv, cx, cy, q, c, s, &bar[b]);
+  };
+  uint32_t phase = 0;
+  auto wait_set = [&](int q) {
+    const int b = q % R_D;
+    mbar_wait(&bar[b], (phase >> b) & 1u);
+    phase ^= 1u << b;
+  };
+  if (tid == 0) {
+    for (int q = 0; q < R_D; ++q) mbar_init(&bar[q], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int q = kb; q <= min(kb + 3, ke); ++q) issue(q);
+  wait_set(kb);
+#pragma unroll 1
+  for (int k = kb; k < ke; ++k) {
+    wait_set(k + 1);
+    const V* S0 = ring + (k % R_D) * 3 * TSV;
+    const V* S1 = ring + ((k + 1) % R_D) * 3 * TSV;
+    acc = cadd(acc, faces_quad<TYV>(C, zih[k - kb], zhd[k - kb], S0, S1, S0 + TSV, S1 + TSV, S0 + 2 * TSV));
+    __syncthreads();   // set k no longer read
+    if (tid == 0 && k + 4 <= ke) {
+      fence_proxy_async();
+      issue(k + 4);
+    }
+  }
+  return VT<V>::cplx(acc);
+}
 
 template <bool PRIME, int TYV = kTYSplit>
 __global__ void __launch_bounds__(Tile<TYV>::NT, 768 / Tile<TYV>::NT)
-    k_delta(const __grid_constant__ SweepArgs A, const __grid_constant__ CUtensorMap tmv) {
-  TEM_TILE_CONSTANTS(TYV);
+    k_delta(const __grid_constant__ SweepArgs A, const __grid_constant__ CUtensorMap tmv,
+            const __grid_constant__ CUtensorMap tmvr) {
+  constexpr int NT = Tile<TYV>::NT;
   extern __shared__ unsigned char smem_raw[];
   double2* ring = smem_align128(smem_raw);   // [R_D][3] tiles
   __shared__ __align__(8) uint64_t bar[R_D];
@@ -825,59 +942,24 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, 768 / Tile<TYV>::NT)
   __shared__ double zih[kMaxChunk];         // ih_z[k]   for k = kb .. ke-1
   __shared__ double zhd[kMaxChunk];         // hdm_z[k]  for k = kb .. ke-1
 
-  const Grid& g = A.g;
   int a, tx0, ty0, kb, ke;
   int pidx;
   block_coords<TYV>(A, a, tx0, ty0, kb, ke, pidx);
   const int tid = threadIdx.x;
   bool live = a < A.ctl->n_active;
   int s = 0;
-  double2 sh = czero();
+  bool real = false;
   if (live) {
     s = A.ctl->list[a];
-    sh = A.st[s].s;
     live = A.st[s].active != 0;
+    real = A.st[s].real != 0;
   }
   double2 acc = czero();
   if (live) {
-    const Column C = make_column<TYV>(g, tx0, ty0);
-    for (int q = tid; q < ke - kb; q += NT) {
-      zih[q] = __ldg(g.ih[2] + kb + q);
-      zhd[q] = __ldg(g.hdm[2] + kb + q);
-    }
-    auto issue = [&](int q) {
-      const int b = q % R_D;
-      mbar_expect_tx(&bar[b], 3 * TILE_BYTES);
-      const int cx = 2 * (tx0 - 1), cy = ty0 - 1;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) tma_tile(ring + (b * 3 + c) * TS2, &tmv, cx, cy, q, c, s, &bar[b]);
-    };
-    uint32_t phase = 0;
-    auto wait_set = [&](int q) {
-      const int b = q % R_D;
-      mbar_wait(&bar[b], (phase >> b) & 1u);
-      phase ^= 1u << b;
-    };
-    if (tid == 0) {
-      for (int q = 0; q < R_D; ++q) mbar_init(&bar[q], 1);
-      fence_barrier_init();
-    }
-    __syncthreads();
-    if (tid == 0)
-      for (int q = kb; q <= min(kb + 3, ke); ++q) issue(q);
-    wait_set(kb);
-#pragma unroll 1
-    for (int k = kb; k < ke; ++k) {
-      wait_set(k + 1);
-      const double2* S0 = ring + (k % R_D) * 3 * TS2;
-      const double2* S1 = ring + ((k + 1) % R_D) * 3 * TS2;
-      acc = cadd(acc, faces_quad<TYV>(C, zih[k - kb], zhd[k - kb], S0, S1, S0 + TS2, S1 + TS2, S0 + 2 * TS2));
-      __syncthreads();   // set k no longer read
-      if (tid == 0 && k + 4 <= ke) {
-        fence_proxy_async();
-        issue(k + 4);
-      }
-    }
+    if (real)
+      acc = delta_body<TYV, double>(A, &tmvr, s, tx0, ty0, kb, ke, ring, bar, zih, zhd);
+    else
+      acc = delta_body<TYV, double2>(A, &tmv, s, tx0, ty0, kb, ke, ring, bar, zih, zhd);
   }
   double rdum = 0.0;
   block_sum_n<NT>(acc, rdum, red);

@@ -37,8 +37,8 @@ def _cplx(z) -> np.ndarray:
     return np.ascontiguousarray(z.view(np.float64).reshape(-1))
 
 
-def _stream_ptr(stream) -> ctypes.c_void_p:
-    s = torch.cuda.current_stream() if stream is None else stream
+def _stream_ptr(stream, device=None) -> ctypes.c_void_p:
+    s = torch.cuda.current_stream(device) if stream is None else stream
     return ctypes.c_void_p(s.cuda_stream)
 
 
@@ -176,13 +176,22 @@ class TemForward:
         return sigma
 
     # ------------------------------------------------------------ calls
+    # Every call runs with the context's device current (the C ABI rejects a
+    # different current device) and on that device's current stream.
+    def _call(self, fn, *args):
+        with torch.cuda.device(self.device):
+            return fn(*args)
+
+    def _stream(self, stream):
+        return _stream_ptr(stream, self.device)
+
     def edge_mass(self, sigma: torch.Tensor, stream=None) -> torch.Tensor:
         _need_cuda(sigma, torch.float64, "sigma")
         if sigma.numel() != self.shape[0] * self.shape[1] * self.shape[2]:
             raise ValueError("sigma size mismatch")
         mass = torch.empty(self.n_slots, dtype=torch.float64, device=self.device)
-        _lib.check(self.lib.tem_edge_mass(self._h, ctypes.c_void_p(sigma.data_ptr()),
-                                          ctypes.c_void_p(mass.data_ptr()), _stream_ptr(stream)))
+        _lib.check(self._call(self.lib.tem_edge_mass, self._h, ctypes.c_void_p(sigma.data_ptr()),
+                              ctypes.c_void_p(mass.data_ptr()), self._stream(stream)))
         return mass
 
     def apply(self, mass: torch.Tensor, shifts, x: torch.Tensor, stream=None) -> torch.Tensor:
@@ -193,9 +202,9 @@ class TemForward:
         if x.shape != (S, self.n_slots):
             raise ValueError(f"x must be (S, n_slots) = {(S, self.n_slots)}")
         y = torch.empty_like(x)
-        _lib.check(self.lib.tem_apply_shifted(self._h, ctypes.c_void_p(mass.data_ptr()), S,
-                                              _dptr(sh), ctypes.c_void_p(x.data_ptr()),
-                                              ctypes.c_void_p(y.data_ptr()), _stream_ptr(stream)))
+        _lib.check(self._call(self.lib.tem_apply_shifted, self._h, ctypes.c_void_p(mass.data_ptr()), S,
+                              _dptr(sh), ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                              self._stream(stream)))
         return y
 
     def workspace(self, S: int) -> torch.Tensor:
@@ -217,14 +226,53 @@ class TemForward:
         work = self.workspace(S)
         iters = np.zeros(S, dtype=np.int32)
         relres = np.zeros(S, dtype=np.float64)
-        rc = self.lib.tem_cocg_solve(self._h, ctypes.c_void_p(mass.data_ptr()),
-                                     ctypes.c_void_p(f.data_ptr()), S, _dptr(sh), float(tol),
-                                     int(maxit), ctypes.c_void_p(x.data_ptr()),
-                                     ctypes.c_void_p(work.data_ptr()), work.numel(),
-                                     _iptr(iters), _dptr(relres), _stream_ptr(stream))
+        rc = self._call(self.lib.tem_cocg_solve, self._h, ctypes.c_void_p(mass.data_ptr()),
+                        ctypes.c_void_p(f.data_ptr()), S, _dptr(sh), float(tol), int(maxit),
+                        ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(work.data_ptr()), work.numel(),
+                        _iptr(iters), _dptr(relres), self._stream(stream))
         if rc != 0 and (raise_on_noconv or rc != _lib.TEM_ENOCONV):
             _lib.check(rc)
         return x, iters, relres
+
+    def cocg_rhs(self, mass: torch.Tensor, rhs: torch.Tensor, shifts, tols, maxit: int = 100000,
+                 stream=None, raise_on_noconv: bool = True):
+        """Per-shift right-hand sides (complex (S, n_slots)) and tolerances
+        (tem_cocg_solve_rhs).  Returns (x, iters, relres)."""
+        _need_cuda(mass, torch.float64, "mass")
+        _need_cuda(rhs, torch.complex128, "rhs")
+        sh = _cplx(shifts)
+        S = sh.size // 2
+        if rhs.shape != (S, self.n_slots):
+            raise ValueError(f"rhs must be (S, n_slots) = {(S, self.n_slots)}")
+        t = np.ascontiguousarray(np.broadcast_to(np.asarray(tols, dtype=np.float64), (S,)))
+        x = torch.empty_like(rhs)
+        work = self.workspace(S)
+        iters = np.zeros(S, dtype=np.int32)
+        relres = np.zeros(S, dtype=np.float64)
+        rc = self._call(self.lib.tem_cocg_solve_rhs, self._h, ctypes.c_void_p(mass.data_ptr()),
+                        ctypes.c_void_p(rhs.data_ptr()), S, _dptr(sh), _dptr(t), int(maxit),
+                        ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(work.data_ptr()), work.numel(),
+                        _iptr(iters), _dptr(relres), self._stream(stream))
+        if rc != 0 and (raise_on_noconv or rc != _lib.TEM_ENOCONV):
+            _lib.check(rc)
+        return x, iters, relres
+
+    def residual(self, mass: torch.Tensor, f: torch.Tensor, shifts, x: torch.Tensor, stream=None):
+        """r_s = f - (K + s M) x_s in double-double (tem_residual).  Returns
+        (r (S, n_slots) complex, ||r_s||_2 per shift)."""
+        _need_cuda(mass, torch.float64, "mass")
+        _need_cuda(f, torch.float64, "f")
+        _need_cuda(x, torch.complex128, "x")
+        sh = _cplx(shifts)
+        S = sh.size // 2
+        if x.shape != (S, self.n_slots):
+            raise ValueError(f"x must be (S, n_slots) = {(S, self.n_slots)}")
+        r = torch.empty_like(x)
+        nrm = np.zeros(S)
+        _lib.check(self._call(self.lib.tem_residual, self._h, ctypes.c_void_p(mass.data_ptr()),
+                              ctypes.c_void_p(f.data_ptr()), S, _dptr(sh), ctypes.c_void_p(x.data_ptr()),
+                              ctypes.c_void_p(r.data_ptr()), _dptr(nrm), self._stream(stream)))
+        return r, nrm
 
     def stats(self) -> dict:
         st = _lib.SolveStats()
@@ -241,9 +289,9 @@ class TemForward:
         r = _cplx(res.T.copy())           # ABI wants [K][S]
         ip = np.ascontiguousarray(np.asarray(is_pair, dtype=np.int32))
         u = torch.empty((K, self.n_slots), dtype=torch.float64, device=self.device)
-        _lib.check(self.lib.tem_synthesize(self._h, S, K, _dptr(r), _iptr(ip),
-                                           ctypes.c_void_p(x.data_ptr()),
-                                           ctypes.c_void_p(u.data_ptr()), _stream_ptr(stream)))
+        _lib.check(self._call(self.lib.tem_synthesize, self._h, S, K, _dptr(r), _iptr(ip),
+                              ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(u.data_ptr()),
+                              self._stream(stream)))
         return u
 
     def dbzdt(self, u: torch.Tensor, receivers, stream=None) -> torch.Tensor:
@@ -256,12 +304,32 @@ class TemForward:
         rec = np.ascontiguousarray(np.asarray(receivers, dtype=np.int32).reshape(-1, 3))
         K, R = u.shape[0], rec.shape[0]
         out = torch.empty((K, R), dtype=torch.float64, device=self.device)
-        _lib.check(self.lib.tem_curl_z(self._h, K, ctypes.c_void_p(u.data_ptr()), R, _iptr(rec),
-                                       ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+        _lib.check(self._call(self.lib.tem_curl_z, self._h, K, ctypes.c_void_p(u.data_ptr()), R, _iptr(rec),
+                              ctypes.c_void_p(out.data_ptr()), self._stream(stream)))
         return out
 
+    @staticmethod
+    def opts(tol: float = 1e-10, maxit: int = 200000, refine: bool | int = False, refine_tol: float = 1e-6,
+             channel_tol: float = 1e-8, safety: float = 100.0) -> "_lib.ForwardOpts":
+        """tem_forward_opts.  refine=True: up to 8 rounds of iterative
+        refinement with the channel-aware stopping rule (R13); an
+        int sets the round limit."""
+        o = _lib.ForwardOpts()
+        o.tol, o.maxit = float(tol), int(maxit)
+        o.max_refine = (8 if refine is True else int(refine)) if refine else 0
+        o.refine_tol, o.channel_tol, o.safety = float(refine_tol), float(channel_tol), float(safety)
+        return o
+
+    def forward_workspace(self, S: int, K: int) -> torch.Tensor:
+        key = ("fwd", S, K)
+        if key not in self._work:
+            nbytes = int(self.lib.tem_forward_workspace_bytes(self._h, S, K))
+            self._work[key] = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        return self._work[key]
+
     def forward_host(self, sigma: np.ndarray, f: np.ndarray, table: RationalTable,
-                     tol: float = 1e-10, maxit: int = 100000, out: np.ndarray | None = None):
+                     tol: float = 1e-10, maxit: int = 100000, out: np.ndarray | None = None,
+                     opts=None, **kw):
         """End-to-end with host buffers (tem_forward_host).  Returns
         (u (K, n_slots) host array, iters, relres)."""
         sig = self.sigma_layout(sigma)
@@ -270,20 +338,44 @@ class TemForward:
         sh = _cplx(table.shifts)
         r = _cplx(table.residues.T.copy())
         ip = np.ascontiguousarray(table.is_pair.astype(np.int32))
+        o = opts if opts is not None else self.opts(tol, maxit, **kw)
         u = np.empty((K, self.n_slots)) if out is None else out
         iters = np.zeros(S, dtype=np.int32)
         relres = np.zeros(S)
-        with torch.cuda.device(self.device):
-            rc = self.lib.tem_forward_host(self._h, _dptr(sig), _dptr(f), S, _dptr(sh), K,
-                                           _dptr(r), _iptr(ip), float(tol), int(maxit),
-                                           _dptr(u), _iptr(iters), _dptr(relres))
+        rc = self._call(self.lib.tem_forward_host, self._h, _dptr(sig), _dptr(f), S, _dptr(sh), K,
+                        _dptr(r), _iptr(ip), ctypes.byref(o), _dptr(u), _iptr(iters), _dptr(relres))
         _lib.check(rc)
         return u, iters, relres
 
+    def forward_stats(self) -> dict:
+        st = _lib.ForwardStats()
+        _lib.check(self.lib.tem_last_forward_stats(self._h, ctypes.byref(st)))
+        return {k: getattr(st, k) for k, _ in _lib.ForwardStats._fields_}
+
     def forward(self, sigma: torch.Tensor, f: torch.Tensor, table: RationalTable,
-                tol: float = 1e-10, maxit: int = 100000, stream=None):
-        """Device-resident forward: mass, COCG, synthesis.  Returns (u, x, iters, relres)."""
+                tol: float = 1e-10, maxit: int = 200000, stream=None, opts=None,
+                raise_on_noconv: bool = True, **kw):
+        """Device-resident forward (tem_forward): mass, COCG, synthesis and,
+        with refine=..., the channel-aware refinement.  Returns
+        (u, x, iters, relres)."""
+        _need_cuda(f, torch.float64, "f")
         mass = self.edge_mass(sigma, stream)
-        x, iters, relres = self.cocg(mass, f, table.shifts, tol, maxit, stream=stream)
-        u = self.synthesize(x, table.residues, table.is_pair, stream)
+        S, K = table.residues.shape
+        sh = _cplx(table.shifts)
+        r = _cplx(table.residues.T.copy())
+        ip = np.ascontiguousarray(table.is_pair.astype(np.int32))
+        o = opts if opts is not None else self.opts(tol, maxit, **kw)
+        x = torch.empty((S, self.n_slots), dtype=torch.complex128, device=self.device)
+        u = torch.empty((K, self.n_slots), dtype=torch.float64, device=self.device)
+        work = self.forward_workspace(S, K)
+        iters = np.zeros(S, dtype=np.int32)
+        relres = np.zeros(S)
+        st = _lib.ForwardStats()
+        rc = self._call(self.lib.tem_forward, self._h, ctypes.c_void_p(mass.data_ptr()),
+                        ctypes.c_void_p(f.data_ptr()), S, _dptr(sh), K, _dptr(r), _iptr(ip), ctypes.byref(o),
+                        ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(u.data_ptr()),
+                        ctypes.c_void_p(work.data_ptr()), work.numel(), _iptr(iters), _dptr(relres),
+                        ctypes.byref(st), self._stream(stream))
+        if rc != 0 and (raise_on_noconv or rc != _lib.TEM_ENOCONV):
+            _lib.check(rc)
         return u, x, iters, relres

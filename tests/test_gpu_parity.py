@@ -342,3 +342,29 @@ def test_curl_z_observation_vs_oracle():
     assert np.all(np.abs(ref[:, 0]) > 0)                       # the loop centre sees a transient
     with pytest.raises(_lib.TemError):
         fw.dbzdt(u, [(nx, 0, 0)])
+
+
+def test_gpu_fields_vs_dense_expm_tiny():
+    """BASELINE configs[0] "also checked against dense expm": the GPU channel
+    fields (tight solve) against brute-force exp(-t_j M^-1 K) b (oracle
+    eigendecomposition, eq:expm P:134-139) obey the M-norm bound of P:210-217,
+        ||u_GPU(t_j) - exp(-t_j M^-1 K) b||_M <= ||b||_M * error_j,
+    at all 31 channels, with error_j = max_x |exp(-t_j x) - r^[j](x)| of the
+    table (eq:error, computed by the oracle fit); the early channels carry
+    real signal, so the comparison is not between zeros."""
+    wl = make_workload("tiny")
+    fw, asm, slots, table, sigma, f = _setup(wl)
+    import json, os
+    meta = json.load(open(os.path.join(os.path.dirname(__file__), "..", "data", "rational", "tiny.json")))
+    errs = np.asarray(meta["channel_errors"])
+    u, x, iters, relres = fw.forward(sigma, f, table, tol=1e-14, maxit=50000)
+    ug = u.cpu().numpy()[:, slots].T                       # (N, K)
+    E = ofw.expm_dense(asm, wl.times)
+    b_M = ofw.m_norm(asm, asm.f / asm.Mdiag)
+    ratios = []
+    for j in range(len(wl.times)):
+        err = ofw.m_norm(asm, ug[:, j] - E[:, j])
+        ratios.append(err / (b_M * errs[j]))
+        assert err <= b_M * errs[j] * (1 + 1e-6) + 1e-12 * b_M, (j, err, b_M * errs[j])
+    assert ofw.m_norm(asm, E[:, 0]) > 10 * b_M * errs[0]
+    print(f"GPU vs dense expm: max ||u-E||_M / (||b||_M err_j) = {max(ratios):.3f}")
