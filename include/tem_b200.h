@@ -202,8 +202,10 @@ int tem_residual(tem_ctx* ctx, const double* mass, const double* f, int S, const
  * Channel-aware stopping: after a round, the change of channel k due to
  * shift s is ||w_s Re(alpha_ks d_s)||_M / ||u_k||_M (the M-norm of the
  * paper's error bound); the error left behind is estimated as that
- * change times min(1, safety * ||r_s after|| / ||r_s before||).  A shift is
- * refined again while some channel's estimate exceeds channel_tol / S; the
+ * change times min(1, safety * ||r_s after|| / ||r_s before||).  The first
+ * round asks every shift for a residual reduction of refine_tol; a shift is
+ * refined again while some channel's estimate exceeds channel_tol / S, asked
+ * for the reduction that brings its estimate to half of that share.  The
  * loop ends when every channel's summed estimate is <= channel_tol (or after
  * max_refine rounds).  u is re-synthesised from the refined x. */
 typedef struct {
@@ -221,8 +223,9 @@ typedef struct {
   double loop_ms;                      /* GPU time of all COCG solves */
   double channel_bound;                /* max_k of the final estimate (-1: no refinement) */
   double relres_max;                   /* max_s final relative residual (double-double if refined) */
+  long long kernel_launches;           /* kernels launched (solves, synthesis, refinement) */
 } tem_forward_stats;
-/* tol 1e-10, maxit 200000, max_refine 0, refine_tol 1e-6, channel_tol 1e-8, safety 100 */
+/* tol 1e-10, maxit 200000, max_refine 0, refine_tol 1e-5, channel_tol 1e-7, safety 4 */
 void tem_forward_default_opts(tem_forward_opts* opts);
 size_t tem_forward_workspace_bytes(const tem_ctx* ctx, int S, int K);
 /*   mass, f: device (tem_edge_mass; real edge vector); shifts, residues
@@ -260,7 +263,8 @@ int tem_forward_host(tem_ctx* ctx, const double* sigma, const double* f, int S,
  *   residues:   complex[m][K]: alpha_ij / t_max, row i = representative pole i
  *   is_pair:    int[m]: 1 if pole i stands for a conjugate pair (weight 2 in eq:rmj)
  *   uniform_error: (may be NULL) eq:uniform_error estimated on a log grid.
- * Deterministic; CPU only; TEM_EINVAL on bad arguments. */
+ * Deterministic; CPU only; TEM_EINVAL on bad arguments, and when the family
+ * would need more than TEM_MAX_SHIFTS systems (m near 64 with real poles). */
 int tem_fit_family(int K, const double* t, const double* w, int m, int iters, int* n_rep,
                    double* shifts, double* residues, int* is_pair, double* uniform_error);
 

@@ -28,7 +28,8 @@ class ForwardStats(ctypes.Structure):
     """tem_forward_stats (include/tem_b200.h)."""
     _fields_ = [("refine_rounds", ctypes.c_int), ("shift_iterations", ctypes.c_longlong),
                 ("initial_shift_iterations", ctypes.c_longlong), ("loop_ms", ctypes.c_double),
-                ("channel_bound", ctypes.c_double), ("relres_max", ctypes.c_double)]
+                ("channel_bound", ctypes.c_double), ("relres_max", ctypes.c_double),
+                ("kernel_launches", ctypes.c_longlong)]
 
 
 _P = ctypes.c_void_p

@@ -127,9 +127,9 @@ __device__ __forceinline__ void init_body(const tem::SweepArgs& A, int s, int b,
     const int a = (int)(slot / cst);
     const long long nv = slot - a * cst;                 // node in this layout
     const long long row = nv / rowp;
-    const int i = (int)(nv - row * rowp);
+    const int i = (int)(nv - row * rowp) - tem::vofs<V>();
     V zv_ = tem::VT<V>::zero();
-    if (i < nx1) {
+    if (i >= 0 && i < nx1) {
       const long long abi = a * g.Nn + row * nx1 + i;    // slot in the ABI layout
       const double m = __ldg(A.mass + abi);
       if (m > 0.0) {
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(256) k_real_out(tem::SweepArgs A, double2* tmp
     const int a = (int)(slot / g.Nn);
     const long long node = slot - a * g.Nn;
     const long long row = node / nx1;
-    xc[slot] = make_double2(tr[a * g.NnP + row * g.px + (node - row * nx1)], 0.0);
+    xc[slot] = make_double2(tr[a * g.NnP + row * g.px + (node - row * nx1) + 1], 0.0);
   }
 }
 
@@ -415,27 +415,47 @@ static void sweep_geometry(const tem_ctx* c, int S, int nslot, tem::SweepArgs& A
   A.nty = (c->g.n[1] + ty - 1) / ty;
   const int per_sm = ty == tem::kTYSplit ? c->per_sm_split : c->per_sm_two;
   const int base = A.ntx * A.nty * nslot;
-  // z-chunk count.  W = CTAs / resident CTAs.  Keep >= 4 waves when the grid
-  // allows (a few slow shifts must still fill the machine), and among those
-  // maximise (wave quantisation W / ceil(W): a partial last wave idles SMs) x
-  // (march efficiency kch / (kch + 3): a CTA fills its plane pipeline, ~3
-  // steps, before it computes).  Large config, 14 shifts: 1344 columns = 9.08
-  // waves of 148 -> 2 chunks of 64 planes, 18.2 waves.
+  // z-chunk count.  W = CTAs / resident CTAs.
+  // Bandwidth regime (some candidate reaches >= 4 waves with >= 8 planes per
+  // chunk): keep >= 4 waves (a few slow shifts must still fill the machine)
+  // and among those maximise (wave quantisation W / ceil(W): a partial last
+  // wave idles SMs) x (march efficiency kch / (kch + 3): a CTA fills its plane
+  // pipeline, ~3 steps, before it computes).  Large config, 14 shifts: 1344
+  // columns = 9.08 waves of 148 -> 2 chunks of 64 planes, 18.2 waves.
+  // Latency regime (small grids, few active shifts: the whole sweep is less
+  // than 4 waves): minimise the critical path, ceil(W) waves of (kch + 3)
+  // plane steps each, down to one plane per chunk -- e.g. `block` with one
+  // shift left: 32 chunks of 1 plane (4 steps) instead of 4 of 8 (11 steps).
   const int nz = c->g.n[2];
   const int nzc_min = (nz + tem::kMaxChunk - 1) / tem::kMaxChunk;
   int nzc = nzc_min;
-  double best = -1.0;
-  bool best_full = false;
+  const double slots_sm = (double)c->num_sms * per_sm;
+  bool bandwidth = false;
   for (int cand = nzc_min; cand <= 32 && (cand == nzc_min || nz / cand >= 8); ++cand) {
     const int kch = (nz + cand - 1) / cand;
     const int nz_eff = (nz + kch - 1) / kch;
-    const double W = (double)base * nz_eff / ((double)c->num_sms * per_sm);
-    const bool full = W >= 4.0;
-    const double score = full ? W / std::ceil(W) * (double)kch / (kch + 3.0) : W;
-    if ((full && !best_full) || (full == best_full && score > best + 1e-9)) {
-      best = score;
-      best_full = full;
-      nzc = cand;
+    bandwidth |= (double)base * nz_eff / slots_sm >= 4.0;
+  }
+  double best = bandwidth ? -1.0 : 1e300;
+  for (int cand = nzc_min; cand <= (bandwidth ? 32 : std::min(nz, 64)); ++cand) {
+    const int kch = (nz + cand - 1) / cand;
+    const int nz_eff = (nz + kch - 1) / kch;
+    if (nz_eff != cand) continue;   // the same chunking as a smaller count
+    const double W = (double)base * nz_eff / slots_sm;
+    if (bandwidth) {
+      if (cand != nzc_min && nz / cand < 8) break;
+      if (W < 4.0) continue;
+      const double score = W / std::ceil(W) * (double)kch / (kch + 3.0);
+      if (score > best + 1e-9) {
+        best = score;
+        nzc = cand;
+      }
+    } else {
+      const double cost = std::ceil(W - 1e-9) * (kch + 3.0);
+      if (cost < best - 1e-9) {
+        best = cost;
+        nzc = cand;
+      }
     }
   }
   if (const char* env = getenv("TEM_FORCE_NZC")) nzc = std::max(nzc_min, atoi(env));  // tests
@@ -494,7 +514,7 @@ static int make_tmap(const tem_ctx* c, int S, const void* base, CUtensorMap* tm,
   const cuuint64_t px = c->g.px, shift_stride = 48 * nx1 * ny1 * nz1;
   const cuuint64_t dims_c[5] = {2 * nx1, ny1, nz1, 3, (cuuint64_t)S};
   const cuuint64_t str_c[4] = {16 * nx1, 16 * nx1 * ny1, 16 * nx1 * ny1 * nz1, shift_stride};
-  const cuuint64_t dims_r[5] = {nx1, ny1, nz1, 3, (cuuint64_t)S};
+  const cuuint64_t dims_r[5] = {nx1 + 1, ny1, nz1, 3, (cuuint64_t)S};   // leading zero column + nodes
   const cuuint64_t str_r[4] = {8 * px, 8 * px * ny1, 8 * px * ny1 * nz1, shift_stride};
   const cuuint32_t box[5] = {(real ? 1u : 2u) * (cuuint32_t)box_x, (cuuint32_t)box_y, 1, 1, 1};
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
@@ -544,7 +564,7 @@ int tem_create(int nx, int ny, int nz, const double* hx, const double* hy, const
   c->g.st[1] = nx + 1;
   c->g.st[2] = (long long)(nx + 1) * (ny + 1);
   c->g.Nn = Nn;
-  c->g.px = (nx + 1 + 1) / 2 * 2;
+  c->g.px = (nx + 2 + 1) / 2 * 2;
   c->g.NnP = (long long)c->g.px * (ny + 1) * (nz + 1);
   // host tables: 1/h and hdual/mu0
   std::vector<double> tab;
@@ -863,15 +883,23 @@ static int solve(tem_ctx* c, const double* mass, const double* f, const double2*
     TEM_CUDA(cudaGetLastError());
     launches += 2;
   }
+  const bool dbg = getenv("TEM_DEBUG_SYNC") != nullptr;   // debugging: locate a failing launch
+#define TEM_DBG(name)                                                                               \
+  if (dbg) {                                                                                        \
+    cudaError_t e_ = cudaStreamSynchronize(stream);                                                 \
+    if (e_ != cudaSuccess) return fail(TEM_ECUDA, std::string(name) + ": " + cudaGetErrorString(e_)); \
+  }
   const int vec_grid = S * std::max(1, std::min(64, (int)((3 * c->g.Nn + 255) / 256)));
   k_init<<<vec_grid, 256, 0, stream>>>(base, P[0], P[1], split ? Z[1] : nullptr, f);
   TEM_CUDA(cudaGetLastError());
+  TEM_DBG("k_init");
   launches += 1;
   int nslot = S;
   Cfg cfg = make_cfg(nslot);
   if (split) {
     tem::k_delta<true><<<cfg.grid, TS::NT, TS::kSmemDelta, stream>>>(cfg.a2[0], tmZ[0], tmZr[0]);   // delta_0
     TEM_CUDA(cudaGetLastError());
+    TEM_DBG("k_delta<true>");
     launches += 1;
   }
 
@@ -882,11 +910,14 @@ static int solve(tem_ctx* c, const double* mass, const double* f, const double2*
   if (int rc = get_graph(cfg, nslot, &graph)) return rc;
   while (done < maxit) {
     const int chunk = std::min(kChunk, maxit - done);
-    if (chunk == kChunk) {  // kChunk is even: parity returns to 0
+    if (chunk == kChunk && !dbg) {  // kChunk is even: parity returns to 0
       TEM_CUDA(cudaGraphLaunch(graph, stream));
     } else {
-      for (int i = 0; i < chunk; ++i) launch_iter(cfg, (done + i) & 1, stream);
-      TEM_CUDA(cudaGetLastError());
+      for (int i = 0; i < chunk; ++i) {
+        launch_iter(cfg, (done + i) & 1, stream);
+        TEM_CUDA(cudaGetLastError());
+        TEM_DBG(((done + i) & 1) ? "iteration (odd)" : "iteration (even)");
+      }
     }
     launches += 2LL * chunk;
     done += chunk;
@@ -910,12 +941,15 @@ static int solve(tem_ctx* c, const double* mass, const double* f, const double2*
   if (split) {
     k_xfix<<<vec_grid, 256, 0, stream>>>(base, P[1]);
     launches += 1;
+    TEM_DBG("k_xfix");
     if (any_real) {   // real-layout x of real shifts -> complex ABI layout (Z[0] as scratch)
       k_real_out<<<vec_grid, 256, 0, stream>>>(base, Z[0], 0);
       k_real_out<<<vec_grid, 256, 0, stream>>>(base, Z[0], 1);
       launches += 2;
     }
     TEM_CUDA(cudaGetLastError());
+    TEM_DBG("k_real_out");
+#undef TEM_DBG
   }
   TEM_CUDA(cudaEventRecord(c->ev1, stream));
   return finish_solve(c, S, st, base.st, stream, launches, grid, nt, iters, relres);
@@ -1138,6 +1172,7 @@ static int forward(tem_ctx* c, const double* mass, const double* f, int S, const
   std::string solve_msg = g_last_error;
   F.shift_iterations = c->stats.shift_iterations;
   F.loop_ms = c->stats.loop_ms;
+  F.kernel_launches = c->stats.kernel_launches + 1;   // + synthesis
   F.initial_shift_iterations = c->stats.shift_iterations;
   const double fnorm = c->last_fnorm;
   if (int rc = synth(c, S, K, residues, is_pair, xc, u, stream)) return rc;
@@ -1148,6 +1183,7 @@ static int forward(tem_ctx* c, const double* mass, const double* f, int S, const
     double* dout = reinterpret_cast<double*>(w + L.out);
     k_channel_mnorm<<<dim3(L.nblk, K), 256, 0, stream>>>(3 * c->g.Nn, mass, u, part);
     TEM_CUDA(cudaGetLastError());
+    F.kernel_launches += 4;   // channel norms, first residual, their two reductions
     std::vector<double> unorm(K);
     if (int rc = rows_to_host(c, part, K, L.nblk, dout, unorm.data(), stream)) return rc;
     for (auto& v : unorm) v = sqrt(v);
@@ -1158,15 +1194,13 @@ static int forward(tem_ctx* c, const double* mass, const double* f, int S, const
     for (int s = 0; s < S; ++s) res_prev[s] = sqrt(res_now[s]);
     // est[s][k]: estimated remaining error of shift s in channel k (relative M-norm)
     std::vector<double> est((size_t)S * K, 0.0);
-    std::vector<double> tols(S);
+    std::vector<double> tols(S, o.refine_tol);
     for (int round = 1; round <= o.max_refine; ++round) {
       // right-hand sides: r for the refined shifts (written by resid_dd), 0 for the others
       std::vector<char> on(S, 0);
       for (int s : list) on[s] = 1;
-      for (int s = 0; s < S; ++s) {
-        tols[s] = o.refine_tol;
+      for (int s = 0; s < S; ++s)
         if (!on[s]) TEM_CUDA(cudaMemsetAsync(r + (size_t)s * 3 * c->g.Nn, 0, vec1, stream));
-      }
       const int rc2 = solve(c, mass, nullptr, r, S, shifts, 0.0, tols.data(), o.maxit, reinterpret_cast<double*>(d),
                             wc, WL, it1.data(), nullptr, stream);
       if (rc2 == TEM_ECUDA || rc2 == TEM_EINVAL) return rc2;
@@ -1177,6 +1211,7 @@ static int forward(tem_ctx* c, const double* mass, const double* f, int S, const
       for (int s = 0; s < S; ++s) it[s] += it1[s];
       F.shift_iterations += c->stats.shift_iterations;
       F.loop_ms += c->stats.loop_ms;
+      F.kernel_launches += c->stats.kernel_launches + 4;   // + update, residual and their two reductions
       F.refine_rounds = round;
       // x += d, and the M-weighted statistics of d
       tem::UpdateArgs U{};
@@ -1192,7 +1227,7 @@ static int forward(tem_ctx* c, const double* mass, const double* f, int S, const
       std::vector<double> dst(4 * n);
       if (int rc = rows_to_host(c, part, 4 * n, L.nblk, dout, dst.data(), stream)) return rc;
       if (int rc = resid_dd(c, mass, f, S, shifts, list, xc, r, L, w, res_now, stream)) return rc;
-      std::vector<int> next;
+      std::vector<double> worst(S, 0.0);
       for (int y = 0; y < n; ++y) {
         const int s = list[y];
         const double rho_after = sqrt(res_now[y]);
@@ -1200,16 +1235,14 @@ static int forward(tem_ctx* c, const double* mass, const double* f, int S, const
         // safety factor for the error-to-residual amplification, R13)
         const double contr = std::min(1.0, o.safety * rho_after / std::max(res_prev[s], 1e-300));
         const double wgt = is_pair[s] ? 2.0 : 1.0;
-        double worst = 0.0;
         for (int k = 0; k < K; ++k) {
           const double ar = residues[2 * ((size_t)k * S + s)], ai = residues[2 * ((size_t)k * S + s) + 1];
           const double q = ar * ar * dst[4 * y] + ai * ai * dst[4 * y + 1] - 2.0 * ar * ai * dst[4 * y + 2];
           const double dk = wgt * sqrt(std::max(q, 0.0)) / std::max(unorm[k], 1e-300);   // |last correction|
           est[(size_t)s * K + k] = dk * contr;
-          worst = std::max(worst, dk * contr);
+          worst[s] = std::max(worst[s], dk * contr);
         }
         res_prev[s] = rho_after;
-        if (worst > o.channel_tol / S) next.push_back(s);
       }
       double bound = 0.0;
       for (int k = 0; k < K; ++k) {
@@ -1218,11 +1251,22 @@ static int forward(tem_ctx* c, const double* mass, const double* f, int S, const
         bound = std::max(bound, b);
       }
       F.channel_bound = bound;
+      if (bound <= o.channel_tol) break;
+      // next round: the shifts whose estimate exceeds their share of the
+      // target, each asked for the residual reduction that brings its
+      // estimate to half its share (at most refine_tol, at least 1e-9)
+      std::vector<int> next;
+      for (int s : list)
+        if (worst[s] > o.channel_tol / S) {
+          next.push_back(s);
+          tols[s] = std::min(o.refine_tol, std::max(1e-9, 0.5 * (o.channel_tol / S) / (o.safety * worst[s])));
+        }
       list = next;
-      if (bound <= o.channel_tol || list.empty()) break;
+      if (list.empty()) break;
     }
     for (int s = 0; s < S; ++s) rr[s] = res_prev[s] / fnorm;
     if (int rc = synth(c, S, K, residues, is_pair, xc, u, stream)) return rc;
+    F.kernel_launches += 1;
   }
   double rmax = 0.0;
   for (int s = 0; s < S; ++s) {
@@ -1255,9 +1299,9 @@ void tem_forward_default_opts(tem_forward_opts* o) {
   o->tol = 1e-10;
   o->maxit = 200000;
   o->max_refine = 0;
-  o->refine_tol = 1e-6;
-  o->channel_tol = 1e-8;
-  o->safety = 100.0;
+  o->refine_tol = 1e-5;
+  o->channel_tol = 1e-7;
+  o->safety = 4.0;
 }
 
 int tem_forward(tem_ctx* c, const double* mass, const double* f, int S, const double* shifts, int K,

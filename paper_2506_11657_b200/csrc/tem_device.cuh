@@ -25,11 +25,15 @@ struct Grid {
   int n[3];               // cells per axis
   long long st[3];        // node strides: 1, nx+1, (nx+1)(ny+1)
   long long Nn;           // nodes
-  // Real-arithmetic shifts keep their COCG vectors as fp64 edge vectors with
-  // the node rows padded to an even length px (so every TMA global stride is
-  // a multiple of 16 B): slot c * NnP + (k (ny+1) + j) px + i, stored at the
-  // start of the shift's complex slot region (8 * 3 NnP <= 16 * 3 Nn bytes).
-  int px;                 // nx + 1 rounded up to even
+  // Real-arithmetic shifts keep their COCG vectors as fp64 edge vectors whose
+  // node rows carry one leading zero column and are padded to an even length
+  // px: slot c * NnP + (k (ny+1) + j) px + i + 1, stored at the start of the
+  // shift's complex slot region (8 * 3 NnP <= 16 * 3 Nn bytes).  Even px
+  // makes every TMA global stride a multiple of 16 B; the leading column
+  // puts the halo tile origin (node tx0 - 1, column tx0) on an even element,
+  // because a TMA box must start on a 16-byte boundary of the innermost
+  // dimension (measured: odd fp64 coordinates fault on sm_100a).
+  int px;                 // nx + 2 rounded up to even
   long long NnP;          // px (ny+1) (nz+1)
   const double* ih[3];    // 1 / h_a[i], i < n_a                     (device)
   const double* hdm[3];   // hdual_a[i] / mu0, i = 0..n_a             (device)

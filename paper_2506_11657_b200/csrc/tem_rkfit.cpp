@@ -545,6 +545,12 @@ extern "C" int tem_fit_family(int K, const double* t, const double* w, int m, in
     return rc;
   }
   *n_rep = (int)px.size();
+  if (*n_rep > TEM_MAX_SHIFTS) {   // the solver's batch limit (real poles need one system each)
+    tem_set_error("tem_fit_family: the family needs " + std::to_string(*n_rep) + " shifted systems (" +
+                  std::to_string(m) + " poles with real ones), more than TEM_MAX_SHIFTS = " +
+                  std::to_string(TEM_MAX_SHIFTS) + "; lower the degree");
+    return TEM_EINVAL;
+  }
   for (size_t q = 0; q < px.size(); ++q) {
     shifts[2 * q] = -px[q].real();       // s = -xi
     shifts[2 * q + 1] = -px[q].imag();

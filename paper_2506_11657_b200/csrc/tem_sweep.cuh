@@ -548,6 +548,11 @@ template <typename V>
 __device__ __forceinline__ int vrow(const Grid& g) {
   if constexpr (VT<V>::kReal) return g.px; else return g.n[0] + 1;
 }
+// column of node i in a row of this layout is i + vofs
+template <typename V>
+__device__ __forceinline__ constexpr int vofs() {
+  return VT<V>::kReal ? 1 : 0;
+}
 
 // ---------------------------------------------------------------- sweeps
 // One kernel for all modes.  Plane sets q = {X(q+1), Y(q+1), Z(q)} of the
@@ -623,7 +628,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
     const bool with_z = q > kb - 2;
     const int ntile = (with_z ? 3 : 2) * (kZ ? 2 : 1);
     mbar_expect_tx(&bar[sx], ntile * TILE_V);
-    const int cx = kW * (tx0 - 1), cy = ty0 - 1;
+    const int cx = kW * (tx0 - 1) + vofs<V>(), cy = ty0 - 1;   // even: 16-byte aligned box origin
     tma_tile(rX + sx * TSV, tmv, cx, cy, q + 1, 0, s, &bar[sx]);
     tma_tile(rY + sx * TSV, tmv, cx, cy, q + 1, 1, s, &bar[sx]);
     if (with_z) tma_tile(rZ + sz * TSV, tmv, cx, cy, q, 2, s, &bar[sx]);
@@ -685,7 +690,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
   V xN[3], zN[3];
   auto load_centre = [&](int k) {
     const long long node = ((long long)k * ny1 + C.j) * nx1 + C.i;
-    const long long nodeV = ((long long)k * ny1 + C.j) * rowp + C.i;
+    const long long nodeV = ((long long)k * ny1 + C.j) * rowp + C.i + vofs<V>();
     const bool ok = C.in_ij && k < g.n[2];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -707,7 +712,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
   // k-2, k-1, k), Z of k-1, k (sets k-1, k); rotated once per step
   int sxm = pmod(kb - 2, R_XY), sx0 = pmod(kb - 1, R_XY), sxp = pmod(kb, R_XY);
   int szm = pmod(kb - 1, R_Z), sz0 = pmod(kb, R_Z);
-  const long long col = (long long)C.j * rowp + C.i;   // own column, component 0, plane 0
+  const long long col = (long long)C.j * rowp + C.i + vofs<V>();   // own column, component 0, plane 0
   const long long plane = (long long)rowp * ny1;
 #pragma unroll 1
   for (int k = kb; k < ke; ++k) {
@@ -897,7 +902,7 @@ __device__ __forceinline__ double2 delta_body(const SweepArgs& A, const CUtensor
   auto issue = [&](int q) {
     const int b = q % R_D;
     mbar_expect_tx(&bar[b], 3 * TILE_V);
-    const int cx = kW * (tx0 - 1), cy = ty0 - 1;
+    const int cx = kW * (tx0 - 1) + vofs<V>(), cy = ty0 - 1;
 #pragma unroll
     for (int c = 0; c < 3; ++c) tma_tile(ring + (b * 3 + c) * TSV, tmv, cx, cy, q, c, s, &bar[b]);
   };

@@ -42,19 +42,22 @@ def shard_shifts(shifts, world: int) -> list[np.ndarray]:
 
 
 def forward_partial(fw, sigma: torch.Tensor, f: torch.Tensor, table, idx, tol: float = 1e-10,
-                    maxit: int = 200000, stream=None):
+                    maxit: int = 200000, stream=None, opts=None):
     """This rank's share of the forward: mass, COCG for the shifts `idx`,
-    synthesis of their contribution to every channel.  Returns
-    (u_partial (K, n_slots) on the device, iters, relres); with no shifts the
-    contribution is zero and no kernel runs."""
+    synthesis of their contribution to every channel (tem_forward; with
+    `opts` refining, the channel-aware rule measures the corrections against
+    this rank's partial channel fields).  Returns (u_partial (K, n_slots) on
+    the device, iters, relres); with no shifts the contribution is zero and no
+    kernel runs."""
+    from .solver import RationalTable
     idx = np.asarray(idx, dtype=np.int64)
     K = table.residues.shape[1]
     if idx.size == 0:
         u = torch.zeros((K, fw.n_slots), dtype=torch.float64, device=fw.device)
         return u, np.zeros(0, np.int32), np.zeros(0)
-    mass = fw.edge_mass(sigma, stream)
-    x, iters, relres = fw.cocg(mass, f, table.shifts[idx], tol, maxit, stream=stream)
-    u = fw.synthesize(x, table.residues[idx], table.is_pair[idx], stream)
+    sub = RationalTable(table.shifts[idx], table.residues[idx], table.is_pair[idx], table.times)
+    u, x, iters, relres = fw.forward(sigma, f, sub, tol=tol, maxit=maxit, stream=stream, opts=opts)
+    del x
     return u, iters, relres
 
 

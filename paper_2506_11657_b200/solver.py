@@ -309,8 +309,8 @@ class TemForward:
         return out
 
     @staticmethod
-    def opts(tol: float = 1e-10, maxit: int = 200000, refine: bool | int = False, refine_tol: float = 1e-6,
-             channel_tol: float = 1e-8, safety: float = 100.0) -> "_lib.ForwardOpts":
+    def opts(tol: float = 1e-10, maxit: int = 200000, refine: bool | int = False, refine_tol: float = 1e-5,
+             channel_tol: float = 1e-7, safety: float = 4.0) -> "_lib.ForwardOpts":
         """tem_forward_opts.  refine=True: up to 8 rounds of iterative
         refinement with the channel-aware stopping rule (R13); an
         int sets the round limit."""

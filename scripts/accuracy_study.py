@@ -27,9 +27,10 @@ def conducting_mask(fw, wl):
 
 
 SETTINGS = [("plain", dict(refine=False)),
-            ("eta1e-4", dict(refine=True, refine_tol=1e-4, channel_tol=1e-8, safety=10.0)),
-            ("eta1e-5", dict(refine=True, refine_tol=1e-5, channel_tol=1e-8, safety=10.0)),
-            ("eta1e-6", dict(refine=True, refine_tol=1e-6, channel_tol=1e-8, safety=10.0))]
+            ("eta1e-2", dict(refine=True, refine_tol=1e-2)),
+            ("eta1e-4", dict(refine=True, refine_tol=1e-4)),
+            ("eta1e-5", dict(refine=True, refine_tol=1e-5)),
+            ("eta1e-6", dict(refine=True, refine_tol=1e-6))]
 only = os.environ.get("SETTINGS")
 if only:
     SETTINGS = [s for s in SETTINGS if s[0] in only.split(",")]
@@ -44,7 +45,7 @@ for name in sys.argv[2:]:
     cond = torch.from_numpy(conducting_mask(fw, wl)).cuda()
     rec = {"unknowns": fw.n_unknowns, "shifts": table.n_shift, "real_shifts": int(np.sum(table.shifts.imag == 0))}
     t0 = time.time()
-    o = fw.opts(tol=1e-10, refine=4, refine_tol=1e-8, channel_tol=1e-13, safety=10.0)
+    o = fw.opts(tol=1e-10, refine=3, refine_tol=1e-8, channel_tol=1e-12, safety=10.0)
     ur, _, it_r, rr_r = fw.forward(sigma, f, table, opts=o)
     torch.cuda.synchronize()
     st = fw.forward_stats()
