@@ -135,6 +135,25 @@ int tem_cocg_solve(tem_ctx* ctx, const double* mass, const double* f, int S,
 int tem_set_solver(tem_ctx* ctx, int solver);
 int tem_get_solver(const tem_ctx* ctx);
 
+/* How the split scheme's iterations are launched (the same per-element
+ * arithmetic; the reduction partials are grouped by each path's own
+ * z-chunking, so iterates agree to rounding, not bit for bit):
+ *   TEM_LAUNCH_GRAPHS: two kernels per iteration (k_sweep<3|4>, k_delta),
+ *     captured as CUDA graphs of 16 iterations -- the bandwidth path;
+ *   TEM_LAUNCH_PERSISTENT: one cooperative kernel (one CTA per SM) runs up
+ *     to 1024 iterations with grid barriers between the passes and the
+ *     per-shift scalar update in the last CTA to arrive -- built for grids
+ *     whose COCG state stays in L2 (the paper's own experiment has 81 174
+ *     unknowns);
+ *   TEM_LAUNCH_AUTO (default): graphs -- measured faster than the persistent
+ *     kernel on every BASELINE grid ("Launch paths").
+ * The two-sweep scheme always uses graphs.  TEM_EINVAL for other values. */
+#define TEM_LAUNCH_AUTO 0
+#define TEM_LAUNCH_GRAPHS 1
+#define TEM_LAUNCH_PERSISTENT 2
+int tem_set_launch_mode(tem_ctx* ctx, int mode);
+int tem_get_launch_mode(const tem_ctx* ctx);
+
 /* Statistics of the last tem_cocg_solve on this context. */
 typedef struct {
   double loop_ms;             /* GPU time (CUDA events) of init + iteration loop */
@@ -143,6 +162,7 @@ typedef struct {
   int iterations;             /* max over shifts */
   int grid, block;            /* launch configuration of the sweep kernels */
   int real_shifts;            /* shifts solved in real arithmetic (split scheme) */
+  int persistent;             /* 1: the iterations ran in k_persist (TEM_LAUNCH_PERSISTENT) */
 } tem_solve_stats;
 int tem_last_solve_stats(const tem_ctx* ctx, tem_solve_stats* out);
 
@@ -199,15 +219,18 @@ int tem_residual(tem_ctx* ctx, const double* mass, const double* f, int S, const
  *   x_s <- COCG(f) to tol;  u = synthesis(x);  then per round, for the shifts
  *   still refined: r_s = f - (K + s M) x_s in double-double arithmetic,
  *   d_s = COCG(r_s) to refine_tol (relative to ||r_s||), x_s += d_s.
- * Channel-aware stopping: after a round, the change of channel k due to
- * shift s is ||w_s Re(alpha_ks d_s)||_M / ||u_k||_M (the M-norm of the
- * paper's error bound); the error left behind is estimated as that
- * change times min(1, safety * ||r_s after|| / ||r_s before||).  The first
- * round asks every shift for a residual reduction of refine_tol; a shift is
- * refined again while some channel's estimate exceeds channel_tol / S, asked
- * for the reduction that brings its estimate to half of that share.  The
- * loop ends when every channel's summed estimate is <= channel_tol (or after
- * max_refine rounds).  u is re-synthesised from the refined x. */
+ * Channel-aware stopping: after a round, shift s's contraction is
+ * c_s = min(1, safety * ||r_s after|| / ||r_s before||) (residual ratio times
+ * an allowance for the error-to-residual amplification), and the error left
+ * in channel k is estimated as ||sum_s w_s c_s Re(alpha_ks d_s)||_M / ||u_k||_M
+ * -- the round's corrections scaled by their contractions and synthesised
+ * with the cancellation of eq:rmj (the M-norm of the paper's bound,
+ * P:210-217).  The first round asks every shift for a residual reduction of
+ * refine_tol; while some channel's estimate exceeds channel_tol, the shifts
+ * whose own correction could still matter are refined again, asked for the
+ * reduction that brings the estimate to half the target.  The loop ends
+ * when every channel's estimate is <= channel_tol (or after max_refine
+ * rounds).  u is re-synthesised from the refined x. */
 typedef struct {
   double tol;          /* COCG tolerance of the first solve (relative residual), e.g. 1e-10 */
   int maxit;           /* COCG iterations per solve, at most */
@@ -225,7 +248,7 @@ typedef struct {
   double relres_max;                   /* max_s final relative residual (double-double if refined) */
   long long kernel_launches;           /* kernels launched (solves, synthesis, refinement) */
 } tem_forward_stats;
-/* tol 1e-10, maxit 200000, max_refine 0, refine_tol 1e-5, channel_tol 1e-7, safety 4 */
+/* tol 1e-10, maxit 200000, max_refine 0, refine_tol 5e-4, channel_tol 1e-7, safety 1.5 */
 void tem_forward_default_opts(tem_forward_opts* opts);
 size_t tem_forward_workspace_bytes(const tem_ctx* ctx, int S, int K);
 /*   mass, f: device (tem_edge_mass; real edge vector); shifts, residues

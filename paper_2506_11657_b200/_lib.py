@@ -15,7 +15,8 @@ _LIB = None
 class SolveStats(ctypes.Structure):
     _fields_ = [("loop_ms", ctypes.c_double), ("kernel_launches", ctypes.c_longlong),
                 ("shift_iterations", ctypes.c_longlong), ("iterations", ctypes.c_int),
-                ("grid", ctypes.c_int), ("block", ctypes.c_int), ("real_shifts", ctypes.c_int)]
+                ("grid", ctypes.c_int), ("block", ctypes.c_int), ("real_shifts", ctypes.c_int),
+                ("persistent", ctypes.c_int)]
 
 
 class ForwardOpts(ctypes.Structure):
@@ -51,6 +52,8 @@ SIGNATURES = {
     "tem_last_solve_stats": ([_P, ctypes.POINTER(SolveStats)], ctypes.c_int),
     "tem_set_solver": ([_P, ctypes.c_int], ctypes.c_int),
     "tem_get_solver": ([_P], ctypes.c_int),
+    "tem_set_launch_mode": ([_P, ctypes.c_int], ctypes.c_int),
+    "tem_get_launch_mode": ([_P], ctypes.c_int),
     "tem_synthesize": ([_P, ctypes.c_int, ctypes.c_int, _D, _I, _P, _P, _P], ctypes.c_int),
     "tem_curl_z": ([_P, ctypes.c_int, _P, ctypes.c_int, _I, _P, _P], ctypes.c_int),
     "tem_cocg_solve_rhs": ([_P, _P, _P, ctypes.c_int, _D, _D, ctypes.c_int, _P, _P, ctypes.c_size_t, _I,
@@ -85,7 +88,11 @@ def load(build_if_missing: bool = True):
         _build.build()
     lib = ctypes.CDLL(path)
     for name, (args, res) in SIGNATURES.items():
-        fn = getattr(lib, name)
+        fn = getattr(lib, name, None)
+        if fn is None and os.environ.get("TEM_LIB"):   # an older build variant (experiments)
+            continue
+        if fn is None:
+            raise ImportError(f"{path} does not export {name}")
         fn.argtypes = args
         fn.restype = res
     _LIB = lib

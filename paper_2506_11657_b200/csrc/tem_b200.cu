@@ -40,6 +40,7 @@
 #include "../../include/tem_b200.h"
 #include "tem_device.cuh"
 #include "tem_sweep.cuh"
+#include "tem_persist.cuh"
 #include "tem_refine.cuh"
 
 using tem::Grid;
@@ -367,11 +368,14 @@ struct tem_ctx {
   tem_solve_stats stats{};
   int per_sm_two = 2;               // resident CTAs per SM of k_sweep<1> (two-sweep geometry)
   int per_sm_split = 1;             // resident CTAs per SM of k_sweep<3> (split geometry)
+  int per_sm_persist = 0;           // resident CTAs per SM of k_persist (0: cannot co-reside)
+  int launch_mode = TEM_LAUNCH_AUTO;
   int solver = TEM_SOLVER_SPLIT;
   int band = 4;                     // tile rows per band of the block order (block_coords), 32x8 tiles
   int band_split = 8;               // the same for the split scheme's 32x12 tiles (measured best)
   int real_arith = 1;               // real shifts in real arithmetic (split scheme; TEM_NO_REAL=1 disables)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;   // loop timing of the last solve
+  int last_persistent = 0;          // the last solve ran k_persist
   double last_fnorm = 0.0;          // ||rhs||_2 of shift 0 of the last solve
   tem_forward_stats fstats{};       // of the last tem_forward / tem_forward_host
   void* pin = nullptr;              // pinned staging of small host arrays
@@ -406,14 +410,15 @@ static int check_device(const tem_ctx* c) {
 // the grid covers ~4 waves of resident CTAs, so that a few remaining
 // (slow-converging) shifts still fill the machine.
 static void sweep_geometry(const tem_ctx* c, int S, int nslot, tem::SweepArgs& A, int* grid,
-                           int ty = tem::kTYTwoSweep) {
+                           int ty = tem::kTYTwoSweep, int per_sm_override = 0) {
   A.g = c->g;
   A.S = S;
   A.nslot = nslot;
   A.band = ty == tem::kTYSplit ? c->band_split : c->band;
   A.ntx = (c->g.n[0] + 32 - 1) / 32;
   A.nty = (c->g.n[1] + ty - 1) / ty;
-  const int per_sm = ty == tem::kTYSplit ? c->per_sm_split : c->per_sm_two;
+  const int per_sm = per_sm_override > 0 ? per_sm_override
+                   : ty == tem::kTYSplit ? c->per_sm_split : c->per_sm_two;
   const int base = A.ntx * A.nty * nslot;
   // z-chunk count.  W = CTAs / resident CTAs.
   // Bandwidth regime (some candidate reaches >= 4 waves with >= 8 planes per
@@ -490,6 +495,7 @@ static int sweep_attrs() {
   TEM_CUDA(cudaFuncSetAttribute(tem::k_sweep<4>, (cudaFuncAttribute)attr, (int)TS::kSmemDirap));
   TEM_CUDA(cudaFuncSetAttribute(tem::k_delta<false>, (cudaFuncAttribute)attr, (int)TS::kSmemDelta));
   TEM_CUDA(cudaFuncSetAttribute(tem::k_delta<true>, (cudaFuncAttribute)attr, (int)TS::kSmemDelta));
+  TEM_CUDA(cudaFuncSetAttribute(tem::k_persist<>, (cudaFuncAttribute)attr, (int)TS::kSmemUpd));
   return TEM_OK;
 }
 
@@ -603,6 +609,7 @@ int tem_create(int nx, int ny, int nz, const double* hx, const double* hy, const
   }
   if (const char* env = getenv("TEM_BAND")) c->band = c->band_split = atoi(env);   // experiments
   if (const char* env = getenv("TEM_NO_REAL")) c->real_arith = atoi(env) ? 0 : 1;  // experiments, tests
+  if (const char* env = getenv("TEM_LAUNCH")) c->launch_mode = atoi(env);            // experiments
   {
     int per_sm = 0;
     using T2 = tem::Tile<tem::kTYTwoSweep>;
@@ -612,6 +619,8 @@ int tem_create(int nx, int ny, int nz, const double* hx, const double* hy, const
     if (e1 == cudaSuccess)
       e1 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tem::k_sweep<3>, TS::NT, TS::kSmemUpd);
     c->per_sm_split = std::max(1, per_sm);
+    if (e1 == cudaSuccess)
+      e1 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->per_sm_persist, tem::k_persist<>, TS::NT, TS::kSmemUpd);
     if (e1 == cudaSuccess) e1 = cudaEventCreate(&c->ev0);
     if (e1 == cudaSuccess) e1 = cudaEventCreate(&c->ev1);
     if (e1 == cudaSuccess) e1 = cudaEventCreateWithFlags(&c->stage_ev, cudaEventDisableTiming);
@@ -681,7 +690,7 @@ int tem_apply_shifted(tem_ctx* c, const double* mass, int S, const double* shift
 }
 
 struct WorkLayout {
-  size_t z, z1, p0, p1, st, ctl, flags, part_c, part_r, part9, total;
+  size_t z, z1, p0, p1, st, ctl, flags, gbar, part_c, part_r, part9, total;
   size_t nparts;
 };
 
@@ -698,6 +707,7 @@ static WorkLayout work_layout(const tem_ctx* c, int S) {
   L.st = o;     o = align_up(o + sizeof(tem::ShiftState) * TEM_MAX_SHIFTS, 256);
   L.ctl = o;    o = align_up(o + sizeof(tem::Control), 256);
   L.flags = o;  o = align_up(o + sizeof(int) * TEM_MAX_SHIFTS, 256);
+  L.gbar = o;   o = align_up(o + 2 * sizeof(unsigned), 256);
   L.part_c = o; o = align_up(o + nparts * sizeof(double2), 256);
   L.part_r = o; o = align_up(o + nparts * sizeof(double), 256);
   L.part9 = o;  o = align_up(o + tem::kSplitPart * nparts * sizeof(double), 256);
@@ -751,10 +761,23 @@ static int finish_solve(tem_ctx* c, int S, std::vector<tem::ShiftState>& st, con
   c->stats.grid = grid;   // with all shifts active
   c->stats.block = block;
   c->stats.real_shifts = n_real;
+  c->stats.persistent = c->last_persistent;
   c->last_fnorm = S > 0 ? st[0].fnorm : 0.0;
   if (status == TEM_EBREAKDOWN) return fail(status, "tem_cocg_solve: COCG breakdown");
   if (status == TEM_ENOCONV) return fail(status, "tem_cocg_solve: not converged within maxit");
   return TEM_OK;
+}
+
+// The persistent loop (tem_persist.cuh) only on request: measured on B200
+// (scripts/launch_modes.py, profiles/r02/launch_modes.json) it is 2-14%
+// slower than the graph path even on grids whose state fits in L2 (tiny,
+// block, layered): a pass is bound by the per-SM plane-step rate of the
+// 12-warp sweep CTAs, not by launch gaps, and the two grid barriers per
+// iteration cost about what the graph's launch gaps do.
+constexpr int kPersistIters = 1024;           // iterations per cooperative launch (host polls between)
+static bool use_persistent(const tem_ctx* c, int S) {
+  if (c->solver != TEM_SOLVER_SPLIT || c->per_sm_persist < 1 || S > tem::kMaxSlots) return false;
+  return c->launch_mode == TEM_LAUNCH_PERSISTENT;
 }
 
 // clears ShiftState::real of shifts whose right-hand side is complex
@@ -906,9 +929,50 @@ static int solve(tem_ctx* c, const double* mass, const double* f, const double2*
   const bool trace = getenv("TEM_TRACE") != nullptr;
   auto t_prev = std::chrono::steady_clock::now();
   int done = 0;
+  c->last_persistent = split && use_persistent(c, S) ? 1 : 0;
+  if (c->last_persistent) {
+    // one cooperative launch runs up to kPersistIters iterations; z-chunking
+    // per active-slot count for one resident CTA per SM (latency regime)
+    tem::PersistArgs PA{};
+    PA.A = base;
+    for (int q = 0; q < 2; ++q) {
+      PA.Z[q] = Z[q];
+      PA.P[q] = P[q];
+    }
+    for (int ns = 1; ns <= S; ++ns) {
+      tem::SweepArgs g0 = base;
+      int gr = 0;
+      sweep_geometry(c, S, ns, g0, &gr, ty, c->per_sm_persist);
+      PA.nzc[ns] = g0.nzc;
+      PA.kchunk[ns] = g0.kchunk;
+    }
+    PA.gbar = reinterpret_cast<unsigned*>(w + L.gbar);
+    TEM_CUDA(cudaMemsetAsync(PA.gbar, 0, 2 * sizeof(unsigned), stream));
+    const int pgrid = c->num_sms * c->per_sm_persist;
+    while (done < maxit) {
+      PA.it0 = done;
+      PA.n_iter = std::min(kPersistIters, maxit - done);
+      void* args[] = {&PA, &tmZ[0], &tmZ[1], &tmP[0], &tmP[1], &tmZr[0], &tmZr[1], &tmPr[0], &tmPr[1]};
+      TEM_CUDA(cudaLaunchCooperativeKernel((const void*)tem::k_persist<>, dim3(pgrid), dim3(TS::NT), args,
+                                           TS::kSmemUpd, stream));
+      TEM_DBG("k_persist");
+      launches += 1;
+      done += PA.n_iter;
+      TEM_CUDA(cudaMemcpyAsync(c->pinned_active, &base.ctl->n_active, sizeof(int), cudaMemcpyDeviceToHost, stream));
+      TEM_CUDA(cudaStreamSynchronize(stream));
+      if (trace) {
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[tem trace] persistent it<=%d grid=%d active=%d launch_ms=%.3f\n", done, pgrid,
+                *c->pinned_active, std::chrono::duration<double, std::milli>(now - t_prev).count());
+        t_prev = now;
+      }
+      if (*c->pinned_active == 0) break;
+    }
+  }
   cudaGraphExec_t graph = nullptr;
-  if (int rc = get_graph(cfg, nslot, &graph)) return rc;
-  while (done < maxit) {
+  if (!c->last_persistent)
+    if (int rc = get_graph(cfg, nslot, &graph)) return rc;
+  while (!c->last_persistent && done < maxit) {
     const int chunk = std::min(kChunk, maxit - done);
     if (chunk == kChunk && !dbg) {  // kChunk is even: parity returns to 0
       TEM_CUDA(cudaGraphLaunch(graph, stream));
@@ -994,6 +1058,17 @@ int tem_set_solver(tem_ctx* c, int solver) {
 }
 
 int tem_get_solver(const tem_ctx* c) { return c ? c->solver : TEM_EINVAL; }
+
+int tem_set_launch_mode(tem_ctx* c, int mode) {
+  if (!c) return fail(TEM_EINVAL, "tem_set_launch_mode: null context");
+  if (mode != TEM_LAUNCH_AUTO && mode != TEM_LAUNCH_GRAPHS && mode != TEM_LAUNCH_PERSISTENT)
+    return fail(TEM_EINVAL, "tem_set_launch_mode: unknown mode " + std::to_string(mode));
+  if (mode == TEM_LAUNCH_PERSISTENT && c->per_sm_persist < 1)
+    return fail(TEM_EINVAL, "tem_set_launch_mode: k_persist cannot be made resident on this device");
+  c->launch_mode = mode;
+  return TEM_OK;
+}
+int tem_get_launch_mode(const tem_ctx* c) { return c ? c->launch_mode : TEM_EINVAL; }
 
 int tem_last_solve_stats(const tem_ctx* c, tem_solve_stats* out) {
   if (!c || !out) return fail(TEM_EINVAL, "tem_last_solve_stats: null pointer");
@@ -1192,8 +1267,6 @@ static int forward(tem_ctx* c, const double* mass, const double* f, int S, const
     std::vector<double> res_prev(S), res_now;
     if (int rc = resid_dd(c, mass, f, S, shifts, list, xc, r, L, w, res_now, stream)) return rc;
     for (int s = 0; s < S; ++s) res_prev[s] = sqrt(res_now[s]);
-    // est[s][k]: estimated remaining error of shift s in channel k (relative M-norm)
-    std::vector<double> est((size_t)S * K, 0.0);
     std::vector<double> tols(S, o.refine_tol);
     for (int round = 1; round <= o.max_refine; ++round) {
       // right-hand sides: r for the refined shifts (written by resid_dd), 0 for the others
@@ -1227,39 +1300,56 @@ static int forward(tem_ctx* c, const double* mass, const double* f, int S, const
       std::vector<double> dst(4 * n);
       if (int rc = rows_to_host(c, part, 4 * n, L.nblk, dout, dst.data(), stream)) return rc;
       if (int rc = resid_dd(c, mass, f, S, shifts, list, xc, r, L, w, res_now, stream)) return rc;
-      std::vector<double> worst(S, 0.0);
+      // per shift: the contraction this round achieved, c_s = min(1, safety *
+      // ||r_s after|| / ||r_s before||) (the residual ratio times an
+      // allowance for the error-to-residual amplification), and the
+      // triangle-inequality size of its correction in each channel
+      std::vector<double> worst(S, 0.0), contr(S, 0.0);
       for (int y = 0; y < n; ++y) {
         const int s = list[y];
         const double rho_after = sqrt(res_now[y]);
-        // contraction of this round ~ the residual ratio it achieved (times a
-        // safety factor for the error-to-residual amplification, R13)
-        const double contr = std::min(1.0, o.safety * rho_after / std::max(res_prev[s], 1e-300));
+        contr[s] = std::min(1.0, o.safety * rho_after / std::max(res_prev[s], 1e-300));
         const double wgt = is_pair[s] ? 2.0 : 1.0;
         for (int k = 0; k < K; ++k) {
           const double ar = residues[2 * ((size_t)k * S + s)], ai = residues[2 * ((size_t)k * S + s) + 1];
           const double q = ar * ar * dst[4 * y] + ai * ai * dst[4 * y + 1] - 2.0 * ar * ai * dst[4 * y + 2];
-          const double dk = wgt * sqrt(std::max(q, 0.0)) / std::max(unorm[k], 1e-300);   // |last correction|
-          est[(size_t)s * K + k] = dk * contr;
-          worst[s] = std::max(worst[s], dk * contr);
+          worst[s] = std::max(worst[s], wgt * sqrt(std::max(q, 0.0)) / std::max(unorm[k], 1e-300));
         }
         res_prev[s] = rho_after;
       }
-      double bound = 0.0;
-      for (int k = 0; k < K; ++k) {
-        double b = 0.0;
-        for (int s = 0; s < S; ++s) b += est[(size_t)s * K + k];
-        bound = std::max(bound, b);
+      // the error left in channel k is estimated as the round's correction of
+      // every shift scaled by that shift's contraction, synthesised with
+      // cancellation: ||sum_s w_s c_s Re(alpha_ks d_s)||_M / ||u_k||_M (per-shift
+      // terms cancel in late channels as the fields do, eq:rmj)
+      {
+        double wts[TEM_MAX_SHIFTS];
+        for (int s = 0; s < S; ++s) wts[s] = (is_pair[s] ? 2.0 : 1.0) * contr[s];
+        const void* src[2] = {residues, wts};
+        const size_t bytes[2] = {(size_t)K * S * sizeof(double2), S * sizeof(double)};
+        if (int rc = stage_to_device(c, src, bytes, 2, stream)) return rc;
+        const char* sc = static_cast<const char*>(c->scratch);
+        const double2* res_d = reinterpret_cast<const double2*>(sc);
+        const double* w_d = reinterpret_cast<const double*>(sc + align_up(bytes[0], 256));
+        tem::k_dsynth_mnorm<<<dim3(L.nblk, (K + tem::kCB - 1) / tem::kCB), 256, 0, stream>>>(
+            3 * c->g.Nn, mass, S, K, res_d, w_d, d, part);
+        TEM_CUDA(cudaGetLastError());
+        F.kernel_launches += 2;
       }
+      std::vector<double> dch(K);
+      if (int rc = rows_to_host(c, part, K, L.nblk, dout, dch.data(), stream)) return rc;
+      double bound = 0.0;
+      for (int k = 0; k < K; ++k) bound = std::max(bound, sqrt(std::max(dch[k], 0.0)) / std::max(unorm[k], 1e-300));
       F.channel_bound = bound;
       if (bound <= o.channel_tol) break;
-      // next round: the shifts whose estimate exceeds their share of the
-      // target, each asked for the residual reduction that brings its
-      // estimate to half its share (at most refine_tol, at least 1e-9)
+      // next round: every shift whose own correction could still matter
+      // (triangle size above its share of the target), each asked for the
+      // residual reduction that brings the estimate to half the target
+      const double eta = std::min(o.refine_tol, std::max(1e-9, 0.5 * o.channel_tol / (o.safety * bound)));
       std::vector<int> next;
       for (int s : list)
-        if (worst[s] > o.channel_tol / S) {
+        if (worst[s] * contr[s] > o.channel_tol / S) {
           next.push_back(s);
-          tols[s] = std::min(o.refine_tol, std::max(1e-9, 0.5 * (o.channel_tol / S) / (o.safety * worst[s])));
+          tols[s] = eta;
         }
       list = next;
       if (list.empty()) break;
@@ -1299,9 +1389,9 @@ void tem_forward_default_opts(tem_forward_opts* o) {
   o->tol = 1e-10;
   o->maxit = 200000;
   o->max_refine = 0;
-  o->refine_tol = 1e-5;
+  o->refine_tol = 5e-4;
   o->channel_tol = 1e-7;
-  o->safety = 4.0;
+  o->safety = 1.5;
 }
 
 int tem_forward(tem_ctx* c, const double* mass, const double* f, int S, const double* shifts, int K,

@@ -245,6 +245,62 @@ __global__ void __launch_bounds__(256) k_channel_mnorm(long long nslots, const d
   }
 }
 
+// Net change of every channel in a refinement round (reading R13): per
+// channel k, ||sum_s w_s Re(res[k][s] d_s)||_M^2 over the correction block d
+// (shift block; d_s = 0 for shifts not refined this round) -> part[k][x].
+// The per-shift contributions cancel in late channels exactly as the
+// channel fields do (eq:rmj), so the NET change, not the sum of |terms|, is
+// the measure of how far the channel moved.  kCB channels per block row
+// (blockIdx.y); d is re-read once per row of channels.
+constexpr int kCB = 8;
+__global__ void __launch_bounds__(256) k_dsynth_mnorm(long long nslots, const double* __restrict__ mass, int S,
+                                                      int K, const double2* __restrict__ res,
+                                                      const double* __restrict__ w, const double2* __restrict__ d,
+                                                      double* part) {
+  __shared__ double2 sres[kCB * 32];
+  const int k0 = blockIdx.y * kCB;
+  for (int i = threadIdx.x; i < kCB * S; i += blockDim.x) {
+    const int c = i / S, s = i - c * S;
+    const double2 a = k0 + c < K ? res[(k0 + c) * S + s] : czero();
+    sres[i] = make_double2(w[s] * a.x, w[s] * a.y);
+  }
+  __syncthreads();
+  double acc[kCB];
+#pragma unroll
+  for (int c = 0; c < kCB; ++c) acc[c] = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nslots;
+       e += (long long)gridDim.x * blockDim.x) {
+    const double m = __ldg(mass + e);
+    if (m == 0.0) continue;
+    double v[kCB];
+#pragma unroll
+    for (int c = 0; c < kCB; ++c) v[c] = 0.0;
+    for (int s = 0; s < S; ++s) {
+      const double2 dv = __ldg(d + (long long)s * nslots + e);
+#pragma unroll
+      for (int c = 0; c < kCB; ++c) {
+        const double2 a = sres[c * S + s];
+        v[c] = fma(a.x, dv.x, fma(-a.y, dv.y, v[c]));
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kCB; ++c) acc[c] = fma(m * v[c], v[c], acc[c]);
+  }
+  __shared__ double red[kCB][8];
+#pragma unroll
+  for (int c = 0; c < kCB; ++c) {
+    double t = acc[c];
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+    if ((threadIdx.x & 31) == 0) red[c][threadIdx.x >> 5] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x < kCB && k0 + (int)threadIdx.x < K) {
+    double t = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[threadIdx.x][q];
+    part[(long long)(k0 + threadIdx.x) * gridDim.x + blockIdx.x] = t;
+  }
+}
+
 // out[row] = sum_b part[row * ncol + b], one warp per row, fixed order.
 __global__ void k_rows_sum(const double* __restrict__ part, int nrow, int ncol, double* out) {
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;

@@ -301,29 +301,24 @@ __device__ __forceinline__ void stencil3p(const Grid& g, const Column& C, int c0
   const double wx = C.cxy * ihz, wx_z = C.cxy * ihzm, wx_y = C.cxym * ihz;      // Fx(m), Fx(m-ez), Fx(m-ey)
   // G = W * circulation (right-hand rule about the face normal), accumulated
   // into (K v)_x = Gz - Gz(m-ey) - Gy + Gy(m-ez), (K v)_y = Gx - Gx(m-ez) - Gz + Gz(m-ex),
-  // (K v)_z = Gy - Gy(m-ex) - Gx + Gx(m-ey) face by face (short live ranges)
-  V qx, qy, qz, G;
-  G = cscale(wz, csub(cadd(x00, T_(Y0, 1, 0)), cadd(T_(X0, 0, 1), y00)));          // Fz(m)
-  qx = G;
-  qy = cscale(-1.0, G);
-  G = cscale(wy, csub(cadd(z00, T_(Xp, 0, 0)), cadd(T_(Z0, 1, 0), x00)));          // Fy(m)
-  qx = csub(qx, G);
-  qz = G;
-  G = cscale(wx, csub(cadd(y00, T_(Z0, 0, 1)), cadd(T_(Yp, 0, 0), z00)));          // Fx(m)
-  qy = cadd(qy, G);
-  qz = csub(qz, G);
-  G = cscale(wz_y, csub(cadd(T_(X0, 0, -1), T_(Y0, 1, -1)), cadd(x00, T_(Y0, 0, -1))));   // Fz(m-ey)
-  qx = csub(qx, G);
-  G = cscale(wy_z, csub(cadd(T_(Zm, 0, 0), x00), cadd(T_(Zm, 1, 0), T_(Xm, 0, 0))));    // Fy(m-ez)
-  qx = cadd(qx, G);
-  G = cscale(wz_x, csub(cadd(T_(X0, -1, 0), y00), cadd(T_(X0, -1, 1), T_(Y0, -1, 0))));   // Fz(m-ex)
-  qy = cadd(qy, G);
-  G = cscale(wx_z, csub(cadd(T_(Ym, 0, 0), T_(Zm, 0, 1)), cadd(y00, T_(Zm, 0, 0))));    // Fx(m-ez)
-  qy = csub(qy, G);
-  G = cscale(wy_x, csub(cadd(T_(Z0, -1, 0), T_(Xp, -1, 0)), cadd(z00, T_(X0, -1, 0))));   // Fy(m-ex)
-  qz = csub(qz, G);
-  G = cscale(wx_y, csub(cadd(T_(Y0, 0, -1), z00), cadd(T_(Yp, 0, -1), T_(Z0, 0, -1))));   // Fx(m-ey)
-  qz = cadd(qz, G);
+  // (K v)_z = Gy - Gy(m-ex) - Gx + Gx(m-ey): the three faces at m serve two
+  // edges each (weight applied once), the six others one edge each (weight
+  // folded into the accumulation, one FMA per component)
+  V qx, qy, qz;
+  {
+    const V Gz = cscale(wz, csub(cadd(x00, T_(Y0, 1, 0)), cadd(T_(X0, 0, 1), y00)));     // Fz(m)
+    const V Gy = cscale(wy, csub(cadd(z00, T_(Xp, 0, 0)), cadd(T_(Z0, 1, 0), x00)));     // Fy(m)
+    const V Gx = cscale(wx, csub(cadd(y00, T_(Z0, 0, 1)), cadd(T_(Yp, 0, 0), z00)));     // Fx(m)
+    qx = csub(Gz, Gy);
+    qy = csub(Gx, Gz);
+    qz = csub(Gy, Gx);
+  }
+  qx = sfma(-wz_y, csub(cadd(T_(X0, 0, -1), T_(Y0, 1, -1)), cadd(x00, T_(Y0, 0, -1))), qx);   // Fz(m-ey)
+  qx = sfma(wy_z, csub(cadd(T_(Zm, 0, 0), x00), cadd(T_(Zm, 1, 0), T_(Xm, 0, 0))), qx);      // Fy(m-ez)
+  qy = sfma(wz_x, csub(cadd(T_(X0, -1, 0), y00), cadd(T_(X0, -1, 1), T_(Y0, -1, 0))), qy);   // Fz(m-ex)
+  qy = sfma(-wx_z, csub(cadd(T_(Ym, 0, 0), T_(Zm, 0, 1)), cadd(y00, T_(Zm, 0, 0))), qy);     // Fx(m-ez)
+  qz = sfma(-wy_x, csub(cadd(T_(Z0, -1, 0), T_(Xp, -1, 0)), cadd(z00, T_(X0, -1, 0))), qz);   // Fy(m-ex)
+  qz = sfma(wx_y, csub(cadd(T_(Y0, 0, -1), z00), cadd(T_(Yp, 0, -1), T_(Z0, 0, -1))), qz);     // Fx(m-ey)
 #undef T_
   E.q[0] = qx;
   E.q[1] = qy;
@@ -366,15 +361,29 @@ __device__ __forceinline__ V faces_quad(const Column& C, double ihz, double hdz,
 //   beta = gamma / gamma_prev,  p^T A p = delta + beta (2 eps + beta mu),
 //   alpha = gamma / p^T A p     (reading R10)
 // PRIME (after k_init): alpha_0 = gamma_0 / delta_0.
+// ShiftState through L2 (ld.global.cg): a persistent CTA must not see an
+// L1 copy of a state another SM's finalisation has since changed.
+__device__ __forceinline__ ShiftState ld_state(const ShiftState* p) {
+  static_assert(sizeof(ShiftState) % 8 == 0, "ShiftState is copied as 8-byte words");
+  ShiftState v;
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(p);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(&v);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(ShiftState) / 8); ++i) dst[i] = __ldcg(src + i);
+  return v;
+}
+__device__ __forceinline__ int ld_cg(const int* p) { return __ldcg(p); }
+
 template <bool PRIME, int TYV>
-__device__ void finalize_split(const SweepArgs& A) {
+__device__ void finalize_split(const SweepArgs& A, int ns, int per) {
+  // ns: shift slots of the pass; per: work units (partials) per slot
   constexpr int NT = Tile<TYV>::NT;
-  const int S = A.S, ns = A.nslot;
-  const int n_list = A.ctl->n_active;
+  const int S = A.S;
+  const int n_list = ld_cg(&A.ctl->n_active);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int per = gridDim.x / ns;   // blocks per shift slot (pidx of block_coords)
   for (int a = warp; a < ns && a < n_list; a += NT / 32) {
-    ShiftState& sq = A.st[A.ctl->list[a]];
+    const int sidx = ld_cg(&A.ctl->list[a]);
+    ShiftState sq = ld_state(&A.st[sidx]);
     if (!sq.active) continue;
     double v[kSplitPart];
 #pragma unroll
@@ -398,6 +407,7 @@ __device__ void finalize_split(const SweepArgs& A) {
         sq.alpha_prev = czero();
         sq.beta = czero();
       }
+      A.st[sidx] = sq;
       continue;
     }
     sq.iters += 1;
@@ -421,12 +431,14 @@ __device__ void finalize_split(const SweepArgs& A) {
         sq.rho = gam;
       }
     }
+    A.st[sidx] = sq;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence();
     int na = 0;
     for (int q = 0; q < S; ++q)
-      if (A.st[q].active) A.ctl->list[na++] = q;
+      if (ld_cg(&A.st[q].active)) A.ctl->list[na++] = q;
     A.ctl->n_active = na;
     A.ctl->ticket[PRIME ? 6 : 5] = 0;
   }
@@ -499,13 +511,13 @@ __device__ void finalize(const SweepArgs& A) {
 // slot-fastest order (slot, then column, then row).  pidx: index of the
 // block's reduction partials, slot-major ([slot][tile and chunk]).
 template <int TYV>
-__device__ __forceinline__ void block_coords(const SweepArgs& A, int& a, int& tx0, int& ty0, int& kb,
-                                             int& ke, int& pidx) {
+__device__ __forceinline__ void unit_coords(const SweepArgs& A, int idx, int ns, int nzc, int kchunk, int& a,
+                                            int& tx0, int& ty0, int& kb, int& ke, int& pidx) {
   constexpr int TX = Tile<TYV>::TX, TY = Tile<TYV>::TY;
-  const int ns = A.nslot, ntx = A.ntx, nty = A.nty;
+  const int ntx = A.ntx, nty = A.nty;
   const int per_z = ns * ntx * nty;
-  const int zc = blockIdx.x / per_z;
-  int r = blockIdx.x - zc * per_z;
+  const int zc = idx / per_z;
+  int r = idx - zc * per_z;
   int tx, ty;
   if (A.band <= 0) {
     a = r % ns;
@@ -524,9 +536,14 @@ __device__ __forceinline__ void block_coords(const SweepArgs& A, int& a, int& tx
   }
   tx0 = tx * TX;
   ty0 = ty * TY;
-  kb = zc * A.kchunk;
-  ke = min(kb + A.kchunk, A.g.n[2]);
-  pidx = a * (A.nzc * ntx * nty) + (zc * nty + ty) * ntx + tx;
+  kb = zc * kchunk;
+  ke = min(kb + kchunk, A.g.n[2]);
+  pidx = a * (nzc * ntx * nty) + (zc * nty + ty) * ntx + tx;
+}
+template <int TYV>
+__device__ __forceinline__ void block_coords(const SweepArgs& A, int& a, int& tx0, int& ty0, int& kb,
+                                             int& ke, int& pidx) {
+  unit_coords<TYV>(A, blockIdx.x, A.nslot, A.nzc, A.kchunk, a, tx0, ty0, kb, ke, pidx);
 }
 
 // ---------------------------------------------------------------- layouts
@@ -568,11 +585,21 @@ struct Partials {
   double r;
 };
 
+// The vectors one sweep reads and writes (per iteration parity).
+struct Bufs {
+  double2* out;          // MODE 0: y; MODE 1, 3, 4: p_new
+  double2* z;            // MODE 2 (in/out); MODE 3, 4: z_{i+1}
+  const double2* zin;    // MODE 4: z_i own values
+  const double2* pold;   // MODE 4: p_{i-1} own values
+};
+__host__ __device__ __forceinline__ Bufs bufs_of(const SweepArgs& A) { return Bufs{A.out, A.z, A.zin, A.pold}; }
+
 template <int MODE, int TYV, typename V>
 __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap* tmv, const CUtensorMap* tmz,
                                            int s, int tx0, int ty0, int kb, int ke, double2 sh2, double2 alpha2,
                                            double2 beta2, double2 alpha_prev2, double2* ring2, uint64_t* bar,
-                                           double* zih, double* zhd, Partials& P) {
+                                           uint32_t& phase, bool init_bars, double* zih, double* zhd, Partials& P,
+                                           const Bufs& B) {
   TEM_TILE_CONSTANTS(TYV);
   constexpr bool kZ = (MODE == 1 || MODE == 3 || MODE == 4);   // p_new = z + beta p_old formed in smem
   constexpr bool kUpd = (MODE == 3 || MODE == 4);               // split pass 1: full update
@@ -611,11 +638,11 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
   const long long cst = vcomp<V>(g);                 // component stride of this layout
   const int rowp = vrow<V>(g);                       // node row pitch of this layout
   const int nx1 = g.n[0] + 1, ny1 = g.n[1] + 1;
-  V* out = vbase<V>(A.out, s, g);
+  V* out = vbase<V>(B.out, s, g);
   V* xv = vbase<V>(A.x, s, g);
-  V* zv = vbase<V>(A.z, s, g);
-  const V* zin = vbase<V>(A.zin, s, g);
-  const V* pold = vbase<V>(A.pold, s, g);
+  V* zv = vbase<V>(B.z, s, g);
+  const V* zin = vbase<V>(B.zin, s, g);
+  const V* pold = vbase<V>(B.pold, s, g);
   for (int q = tid; q <= ke - kb; q += NT) {
     const int k = kb - 1 + q;
     zih[q] = k >= 0 ? __ldg(g.ih[2] + k) : 0.0;
@@ -639,7 +666,8 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
       if (with_z) tma_tile(d + 2 * TSV, tmz, cx, cy, q, 2, s, &bar[sx]);
     }
   };
-  uint32_t phase = 0;   // bit b = parity of the next wait on bar[b]
+  // phase: bit b = parity of the next wait on bar[b] (kept across the work
+  // units of a persistent CTA; every unit waits for every set it issues)
   auto wait_set = [&](int q) {
     const int b = pmod(q, R_XY);
     mbar_wait(&bar[b], (phase >> b) & 1u);
@@ -660,8 +688,11 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
     }
   };
   if (tid == 0) {
-    for (int q = 0; q < R_XY; ++q) mbar_init(&bar[q], 1);
-    fence_barrier_init();
+    if (init_bars) {
+      for (int q = 0; q < R_XY; ++q) mbar_init(&bar[q], 1);
+      fence_barrier_init();
+    }
+    fence_proxy_async();   // persistent CTA: the previous unit's generic smem accesses before the TMA writes
   }
   __syncthreads();
   if (!kZ) {
@@ -701,7 +732,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
         zN[c] = ok ? zv[slot] : VT<V>::zero();
       }
       if (MODE == 4) {
-        xN[c] = ok ? xv[slot] : VT<V>::zero();
+        xN[c] = ok ? __ldcg(xv + slot) : VT<V>::zero();
         zN[c] = ok ? __ldcg(zin + slot) : VT<V>::zero();
       }
     }
@@ -742,7 +773,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
       if (kUpd) {
         const V D = VT<V>::make(E.kd[c] + mN[c] * sh2.x, mN[c] * sh2.y);
         double nD;                                                      // |D|^2
-        const V zn = csub(zN[c], cmul(alpha, cmul(q, crcp(D, nD))));   // z_i - alpha D^-1 A p_i
+        const V zn = csub(zN[c], cmul(alpha, cmul(q, crcp_pc(D, nD))));   // z_i - alpha D^-1 A p_i
         st_stream(out + e, E.p[c]);                                     // p_i
         st_stream(zv + e, zn);                                          // z_{i+1}
         if (MODE == 4) {   // x_{i+1} = x_{i-1} + alpha_{i-1} p_{i-1} + alpha_i p_i
@@ -752,7 +783,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
             st_stream(xv + e, cfma(xc_z, zN[c], cfma(xc_p, E.p[c], xN[c])));
         }
         const V zq = csq(zn);                                           // z_{i+1}^2
-        acc_c = cfma(D, zq, acc_c);                  // gamma_{i+1} = (D z)^T z
+        acc_c = sfma(E.kd[c], zq, acc_c);            // gamma_{i+1} = (D z)^T z = sum kd z^2 + s z^T M z
         acc_r = fma(nD, cabs2(zn), acc_r);           // ||D z||^2
         acc_q = sfma(mN[c], zq, acc_q);              // z^T M z
         acc_e = cfma(zn, q, acc_e);                  // z_{i+1}^T A p_i
@@ -782,11 +813,36 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
       issue(k + 3);
     }
   }
-  P.c = VT<V>::cplx(acc_c);
+  // gamma = sum (kd + s m) z^2: the mass part s z^T M z is acc_q (MODE 3/4)
+  P.c = kUpd ? cadd(VT<V>::cplx(acc_c), cmul(sh2, VT<V>::cplx(acc_q))) : VT<V>::cplx(acc_c);
   P.e = VT<V>::cplx(acc_e);
   P.m = VT<V>::cplx(acc_m);
   P.q = VT<V>::cplx(acc_q);
   P.r = acc_r;
+}
+
+// Split pass 1: the CTA's partial sums (gamma, eps, mu, ||r||^2, s z^T M z)
+// -> A.part[t][pidx] (fixed-order block reduction, deterministic).
+template <int NT>
+__device__ __forceinline__ void write_split_partials(const SweepArgs& A, const Partials& P, double2 sh, int pidx) {
+  __shared__ double red9[kSplitPart * NT / 32];
+  const int tid = threadIdx.x;
+  const double2 dm = cmul(sh, P.q);   // s z^T M z
+  double v[kSplitPart] = {P.c.x, P.c.y, P.e.x, P.e.y, P.m.x, P.m.y, P.r, 0.0, 0.0, dm.x, dm.y};
+#pragma unroll
+  for (int t = 0; t < kSplitPart; ++t)
+    if (t < 7 || t > 8)
+      for (int o = 16; o > 0; o >>= 1) v[t] += __shfl_down_sync(0xffffffffu, v[t], o);
+  const int w = tid >> 5, l = tid & 31;
+  __syncthreads();
+  if (l == 0)
+    for (int t = 0; t < kSplitPart; ++t) red9[kSplitPart * w + t] = v[t];
+  __syncthreads();
+  if (tid < kSplitPart && (tid < 7 || tid > 8)) {
+    double acc = 0.0;
+    for (int q = 0; q < NT / 32; ++q) acc += red9[kSplitPart * q + tid];
+    A.part[tid * A.pstride + pidx] = acc;
+  }
 }
 
 // tmv/tmz: tensor maps of the swept vector and of z over complex shift
@@ -830,38 +886,24 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
     }
   }
   Partials P{};
+  uint32_t phase = 0;
+  const Bufs B = bufs_of(A);
   if (live) {
     if constexpr (kUpd) {
       if (real)
         sweep_body<MODE, TYV, double>(A, &tmvr, &tmzr, s, tx0, ty0, kb, ke, sh, alpha, beta, alpha_prev,
-                                      ring, bar, zih, zhd, P);
+                                      ring, bar, phase, true, zih, zhd, P, B);
       else
         sweep_body<MODE, TYV, double2>(A, &tmv, &tmz, s, tx0, ty0, kb, ke, sh, alpha, beta, alpha_prev,
-                                       ring, bar, zih, zhd, P);
+                                       ring, bar, phase, true, zih, zhd, P, B);
     } else {
       sweep_body<MODE, TYV, double2>(A, &tmv, &tmz, s, tx0, ty0, kb, ke, sh, alpha, beta, alpha_prev, ring,
-                                     bar, zih, zhd, P);
+                                     bar, phase, true, zih, zhd, P, B);
     }
   }
   if (MODE == 0) return;
   if (kUpd) {
-    __shared__ double red9[kSplitPart * NT / 32];
-    const double2 dm = cmul(sh, P.q);   // s z^T M z
-    double v[kSplitPart] = {P.c.x, P.c.y, P.e.x, P.e.y, P.m.x, P.m.y, P.r, 0.0, 0.0, dm.x, dm.y};
-#pragma unroll
-    for (int t = 0; t < kSplitPart; ++t)
-      if (t < 7 || t > 8)
-        for (int o = 16; o > 0; o >>= 1) v[t] += __shfl_down_sync(0xffffffffu, v[t], o);
-    const int w = tid >> 5, l = tid & 31;
-    __syncthreads();
-    if (l == 0)
-      for (int t = 0; t < kSplitPart; ++t) red9[kSplitPart * w + t] = v[t];
-    __syncthreads();
-    if (tid < kSplitPart && (tid < 7 || tid > 8)) {
-      double acc = 0.0;
-      for (int q = 0; q < NT / 32; ++q) acc += red9[kSplitPart * q + tid];
-      A.part[tid * A.pstride + pidx] = acc;
-    }
+    write_split_partials<NT>(A, P, sh, pidx);
     return;
   }
   double2 acc_c = P.c;
@@ -885,7 +927,7 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
 template <int TYV, typename V>
 __device__ __forceinline__ double2 delta_body(const SweepArgs& A, const CUtensorMap* tmv, int s, int tx0,
                                               int ty0, int kb, int ke, double2* ring2, uint64_t* bar,
-                                              double* zih, double* zhd) {
+                                              uint32_t& phase, bool init_bars, double* zih, double* zhd) {
   TEM_TILE_CONSTANTS(TYV);
   constexpr int kW = sizeof(V) / 8;
   constexpr int TSV = TS2 * 2 / kW;
@@ -906,15 +948,17 @@ __device__ __forceinline__ double2 delta_body(const SweepArgs& A, const CUtensor
 #pragma unroll
     for (int c = 0; c < 3; ++c) tma_tile(ring + (b * 3 + c) * TSV, tmv, cx, cy, q, c, s, &bar[b]);
   };
-  uint32_t phase = 0;
   auto wait_set = [&](int q) {
     const int b = q % R_D;
     mbar_wait(&bar[b], (phase >> b) & 1u);
     phase ^= 1u << b;
   };
   if (tid == 0) {
-    for (int q = 0; q < R_D; ++q) mbar_init(&bar[q], 1);
-    fence_barrier_init();
+    if (init_bars) {
+      for (int q = 0; q < R_D; ++q) mbar_init(&bar[q], 1);
+      fence_barrier_init();
+    }
+    fence_proxy_async();
   }
   __syncthreads();
   if (tid == 0)
@@ -960,11 +1004,12 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, 768 / Tile<TYV>::NT)
     real = A.st[s].real != 0;
   }
   double2 acc = czero();
+  uint32_t phase = 0;
   if (live) {
     if (real)
-      acc = delta_body<TYV, double>(A, &tmvr, s, tx0, ty0, kb, ke, ring, bar, zih, zhd);
+      acc = delta_body<TYV, double>(A, &tmvr, s, tx0, ty0, kb, ke, ring, bar, phase, true, zih, zhd);
     else
-      acc = delta_body<TYV, double2>(A, &tmv, s, tx0, ty0, kb, ke, ring, bar, zih, zhd);
+      acc = delta_body<TYV, double2>(A, &tmv, s, tx0, ty0, kb, ke, ring, bar, phase, true, zih, zhd);
   }
   double rdum = 0.0;
   block_sum_n<NT>(acc, rdum, red);
@@ -973,7 +1018,7 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, 768 / Tile<TYV>::NT)
     A.part[8 * A.pstride + pidx] = acc.y;
   }
   if (!last_block(&A.ctl->ticket[PRIME ? 6 : 5])) return;
-  finalize_split<PRIME, TYV>(A);
+  finalize_split<PRIME, TYV>(A, A.nslot, gridDim.x / A.nslot);
 }
 
 }  // namespace tem

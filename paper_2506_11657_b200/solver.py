@@ -139,6 +139,20 @@ class TemForward:
             raise ValueError(f"solver must be one of {sorted(self.SOLVERS)}")
         _lib.check(self.lib.tem_set_solver(self._h, self.SOLVERS[name]))
 
+    LAUNCH_MODES = {"auto": 0, "graphs": 1, "persistent": 2}   # TEM_LAUNCH_* (include/tem_b200.h)
+
+    @property
+    def launch_mode(self) -> str:
+        """How the split scheme's iterations are launched (tem_set_launch_mode)."""
+        code = int(self.lib.tem_get_launch_mode(self._h))
+        return {v: k for k, v in self.LAUNCH_MODES.items()}[code]
+
+    @launch_mode.setter
+    def launch_mode(self, name: str):
+        if name not in self.LAUNCH_MODES:
+            raise ValueError(f"launch_mode must be one of {sorted(self.LAUNCH_MODES)}")
+        _lib.check(self.lib.tem_set_launch_mode(self._h, self.LAUNCH_MODES[name]))
+
     def close(self):
         if self._h:
             self.lib.tem_destroy(self._h)
@@ -309,8 +323,8 @@ class TemForward:
         return out
 
     @staticmethod
-    def opts(tol: float = 1e-10, maxit: int = 200000, refine: bool | int = False, refine_tol: float = 1e-5,
-             channel_tol: float = 1e-7, safety: float = 4.0) -> "_lib.ForwardOpts":
+    def opts(tol: float = 1e-10, maxit: int = 200000, refine: bool | int = False, refine_tol: float = 5e-4,
+             channel_tol: float = 1e-7, safety: float = 1.5) -> "_lib.ForwardOpts":
         """tem_forward_opts.  refine=True: up to 8 rounds of iterative
         refinement with the channel-aware stopping rule (R13); an
         int sets the round limit."""

@@ -26,11 +26,20 @@ def conducting_mask(fw, wl):
     return ~np.concatenate([k > ks, k > ks, k >= ks])
 
 
-SETTINGS = [("plain", dict(refine=False)),
+SETTINGS = [("default", dict(tol=1e-12, refine=True)),
+            ("t11", dict(tol=1e-11, refine=True)),
+            ("t12eta1e-2", dict(tol=1e-12, refine=True, refine_tol=1e-2)),
+            ("plain", dict(refine=False)),
+            ("plain1e-11", dict(tol=1e-11, refine=False)),
+            ("plain1e-12", dict(tol=1e-12, refine=False)),
+            ("plain1e-13", dict(tol=1e-13, refine=False)),
+            ("plain1e-14", dict(tol=1e-14, refine=False)),
+            ("t12eta1e-2x1", dict(tol=1e-12, refine=1, refine_tol=1e-2)),
+            ("t12eta1e-3x1", dict(tol=1e-12, refine=1, refine_tol=1e-3)),
+            ("t13eta1e-2x1", dict(tol=1e-13, refine=1, refine_tol=1e-2)),
             ("eta1e-2", dict(refine=True, refine_tol=1e-2)),
-            ("eta1e-4", dict(refine=True, refine_tol=1e-4)),
-            ("eta1e-5", dict(refine=True, refine_tol=1e-5)),
-            ("eta1e-6", dict(refine=True, refine_tol=1e-6))]
+            ("eta1e-3", dict(refine=True, refine_tol=1e-3)),
+            ("eta1e-5", dict(refine=True, refine_tol=1e-5))]
 only = os.environ.get("SETTINGS")
 if only:
     SETTINGS = [s for s in SETTINGS if s[0] in only.split(",")]
@@ -55,12 +64,16 @@ for name in sys.argv[2:]:
     for label, kw in SETTINGS:
         torch.cuda.synchronize()
         t0 = time.time()
-        u, x, it, rr = fw.forward(sigma, f, table, tol=1e-10, **kw)
+        kw = dict(kw)
+        kw.setdefault("tol", 1e-10)
+        u, x, it, rr = fw.forward(sigma, f, table, raise_on_noconv=False, **kw)
+        r_dd = fw.residual(fw.edge_mass(sigma), f, table.shifts, x)[1] / float(torch.linalg.vector_norm(f))
         torch.cuda.synchronize()
         dt = time.time() - t0
         st = fw.forward_stats()
         err = (torch.linalg.vector_norm((u - ur)[:, cond], dim=1) / urn).cpu().numpy()
         row = {"s": dt, "stats": st, "iters": it.tolist(), "max_err": float(err.max()),
+               "true_relres_dd": r_dd.tolist(),
                "argmax": int(err.argmax()), "n_over_1e-7": int((err > 1e-7).sum()),
                "err_by_channel": err.tolist(), "solver_stats": fw.stats()}
         rec[label] = row

@@ -215,11 +215,9 @@ def test_refined_forward_vs_exact_lu(name):
 
 
 def _oracle_cocg_parallel(asm, shifts, tol):
-    from concurrent.futures import ProcessPoolExecutor
-    from oracle import cocg as ocg
-    with ProcessPoolExecutor(max_workers=min(len(shifts), os.cpu_count() or 1)) as ex:
-        futs = [ex.submit(ocg.cocg, asm, complex(s), tol, 200000) for s in shifts]
-        return np.stack([fu.result()[0] for fu in futs], axis=1)
+    from oracle_pool import cocg_shifts
+    print(f"oracle COCG on {os.cpu_count()} cores")
+    return cocg_shifts(asm, shifts, tol)[0]
 
 
 def test_block_multitile_channels_vs_oracle_cocg():
@@ -235,11 +233,15 @@ def test_block_multitile_channels_vs_oracle_cocg():
     Xo = _oracle_cocg_parallel(asm, table.shifts, 1e-13)
     Uo = ofw.synthesize(Xo, table.residues, table.is_pair)
     cond = _conducting(asm, wl)
-    u, x, iters, relres = _refined(fw, sigma, f, table)
-    err = _channel_err(u.cpu().numpy()[:, slots].T, Uo, cond)
-    u0, _, _, _ = fw.forward(sigma, f, table, tol=1e-10)
-    err0 = _channel_err(u0.cpu().numpy()[:, slots].T, Uo, cond)
-    st = fw.forward_stats()
-    print(f"[block] refined max channel err {err.max():.2e} (unrefined 1e-10: {err0.max():.2e}, "
-          f"{int(np.sum(err0 > 1e-7))} channels > 1e-7)")
-    assert np.all(err <= 1e-7), (err.max(), int(np.argmax(err)))
+    for mode in ("persistent", "graphs"):          # both launch paths of the split scheme
+        fw.launch_mode = mode
+        u, x, iters, relres = _refined(fw, sigma, f, table)
+        assert fw.stats()["persistent"] == (mode == "persistent")
+        err = _channel_err(u.cpu().numpy()[:, slots].T, Uo, cond)
+        st = fw.forward_stats()
+        u0, _, _, _ = fw.forward(sigma, f, table, tol=1e-10)
+        err0 = _channel_err(u0.cpu().numpy()[:, slots].T, Uo, cond)
+        print(f"[block, {mode}] refined max channel err {err.max():.2e} ({st['refine_rounds']} rounds, "
+              f"bound {st['channel_bound']:.1e}); unrefined 1e-10: {err0.max():.2e}, "
+              f"{int(np.sum(err0 > 1e-7))} channels > 1e-7")
+        assert np.all(err <= 1e-7), (mode, err.max(), int(np.argmax(err)))
