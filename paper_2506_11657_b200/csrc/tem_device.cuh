@@ -65,18 +65,6 @@ __device__ __forceinline__ double2 crcp(double2 b, double& n) {
   r = fma(r, fma(-n, r, 1.0), r);
   return make_double2(b.x * r, -b.y * r);
 }
-// The Jacobi preconditioner's 1/D: the seed and ONE Newton step (relative
-// error ~2^-44).  A preconditioner need not be the exact inverse of D, only
-// the same fixed diagonal every iteration, which this deterministic function
-// of D is; the recursion's r = D z then carries the same ~1e-13 relative
-// perturbation as using D~ = 1/rcp(D) would, far below the solve tolerances.
-__device__ __forceinline__ double2 crcp_pc(double2 b, double& n) {
-  n = fma(b.x, b.x, b.y * b.y);
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(n));
-  r = fma(r, fma(-n, r, 1.0), r);
-  return make_double2(b.x * r, -b.y * r);
-}
 __device__ __forceinline__ double2 crcp(double2 b) {
   double n;
   return crcp(b, n);
@@ -101,12 +89,6 @@ __device__ __forceinline__ double crcp(double b, double& n) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
   r = fma(r, fma(-b, r, 1.0), r);
-  return fma(r, fma(-b, r, 1.0), r);
-}
-__device__ __forceinline__ double crcp_pc(double b, double& n) {
-  n = b * b;
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
   return fma(r, fma(-b, r, 1.0), r);
 }
 

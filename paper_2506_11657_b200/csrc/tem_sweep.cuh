@@ -773,7 +773,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
       if (kUpd) {
         const V D = VT<V>::make(E.kd[c] + mN[c] * sh2.x, mN[c] * sh2.y);
         double nD;                                                      // |D|^2
-        const V zn = csub(zN[c], cmul(alpha, cmul(q, crcp_pc(D, nD))));   // z_i - alpha D^-1 A p_i
+        const V zn = csub(zN[c], cmul(alpha, cmul(q, crcp(D, nD))));   // z_i - alpha D^-1 A p_i
         st_stream(out + e, E.p[c]);                                     // p_i
         st_stream(zv + e, zn);                                          // z_{i+1}
         if (MODE == 4) {   // x_{i+1} = x_{i-1} + alpha_{i-1} p_{i-1} + alpha_i p_i

@@ -194,14 +194,22 @@ def _refined(fw, sigma, f, table, **kw):
     return fw.forward(sigma, f, table, opts=o)
 
 
-@pytest.mark.parametrize("name", ["tiny", "ragged", "ragged2"])
+@pytest.mark.parametrize("name", ["tiny", "ragged", "ragged2", "tiny-fit", "ragged-fit"])
 def test_refined_forward_vs_exact_lu(name):
     """North-star bar with the solver at 1e-10: the refined channels match the
     oracle's exact LU within 1e-7 (relative L2, conducting edges) at every
-    channel; the library's own bound is below its target."""
+    channel; the library's own bound is below its target.  `-fit`: the
+    family is the PRODUCT's own host fit (tem_fit_family, the one bench.py
+    uses), handed to both sides -- the field bar holds for it, not only for
+    the oracle's committed tables."""
+    fit = name.endswith("-fit")
+    name = name[:-4] if fit else name
     wl = make_workload("tiny") if name == "tiny" else (
         make_custom(11, 6, 7, seed=2) if name == "ragged" else make_custom(13, 9, 5, seed=5, n_air=1))
-    table = RationalTable.load("tiny") if name == "tiny" else _oracle_table(wl)
+    if fit:
+        table = RationalTable.fit(wl.times, wl.n_poles)
+    else:
+        table = RationalTable.load("tiny") if name == "tiny" else _oracle_table(wl)
     fw, asm, slots, sigma, f = _setup(wl, table)
     u, x, iters, relres = _refined(fw, sigma, f, table)
     st = fw.forward_stats()
