@@ -220,8 +220,11 @@ int tem_residual(tem_ctx* ctx, const double* mass, const double* f, int S, const
  *   still refined: r_s = f - (K + s M) x_s in double-double arithmetic,
  *   d_s = COCG(r_s) to refine_tol (relative to ||r_s||), x_s += d_s.
  * Channel-aware stopping: after a round, shift s's contraction is
- * c_s = min(1, safety * ||r_s after|| / ||r_s before||) (residual ratio times
- * an allowance for the error-to-residual amplification), and the error left
+ * c_s = min(1, safety * max(eta_s, (||r_s after|| - floor_s) / ||r_s before||))
+ * -- eta_s the reduction its correction solve achieved, floor_s =
+ * 2^-52 || |K + s M| |x_s| || the part of the residual explained by the
+ * rounding of x_s itself, safety an allowance for the error-to-residual
+ * amplification -- and the error left
  * in channel k is estimated as ||sum_s w_s c_s Re(alpha_ks d_s)||_M / ||u_k||_M
  * -- the round's corrections scaled by their contractions and synthesised
  * with the cancellation of eq:rmj (the M-norm of the paper's bound,

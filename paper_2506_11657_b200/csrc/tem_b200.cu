@@ -1209,7 +1209,7 @@ static int rows_to_host(tem_ctx* c, const double* part, int nrow, int ncol, doub
 
 static int resid_dd(tem_ctx* c, const double* mass, const double* f, int S, const double* shifts,
                     const std::vector<int>& list, const double2* x, double2* r, const FwdLayout& L, char* w,
-                    std::vector<double>& res2, cudaStream_t stream) {
+                    std::vector<double>& res2, cudaStream_t stream, std::vector<double>* abs2 = nullptr) {
   tem::ResidArgs A{};
   A.g = c->g;
   A.mass = mass;
@@ -1218,14 +1218,20 @@ static int resid_dd(tem_ctx* c, const double* mass, const double* f, int S, cons
   A.r = r;
   A.part = reinterpret_cast<double*>(w + L.part);
   const int n = (int)list.size();
+  A.part_abs = abs2 ? A.part + (size_t)n * L.nblk : nullptr;
   for (int y = 0; y < n; ++y) {
     A.list[y] = list[y];
     A.shifts[y] = make_double2(shifts[2 * list[y]], shifts[2 * list[y] + 1]);
   }
   tem::k_resid_dd<<<dim3(L.nblk, n), 256, 0, stream>>>(A);
   TEM_CUDA(cudaGetLastError());
-  res2.assign(n, 0.0);
-  return rows_to_host(c, A.part, n, L.nblk, reinterpret_cast<double*>(w + L.out), res2.data(), stream);
+  std::vector<double> both(abs2 ? 2 * n : n, 0.0);
+  if (int rc = rows_to_host(c, A.part, (int)both.size(), L.nblk, reinterpret_cast<double*>(w + L.out), both.data(),
+                           stream))
+    return rc;
+  res2.assign(both.begin(), both.begin() + n);
+  if (abs2) abs2->assign(both.begin() + n, both.end());
+  return TEM_OK;
 }
 
 static int forward(tem_ctx* c, const double* mass, const double* f, int S, const double* shifts, int K,
@@ -1274,8 +1280,9 @@ static int forward(tem_ctx* c, const double* mass, const double* f, int S, const
       for (int s : list) on[s] = 1;
       for (int s = 0; s < S; ++s)
         if (!on[s]) TEM_CUDA(cudaMemsetAsync(r + (size_t)s * 3 * c->g.Nn, 0, vec1, stream));
+      std::vector<double> eta(S, 0.0);   // residual reduction each correction solve achieved
       const int rc2 = solve(c, mass, nullptr, r, S, shifts, 0.0, tols.data(), o.maxit, reinterpret_cast<double*>(d),
-                            wc, WL, it1.data(), nullptr, stream);
+                            wc, WL, it1.data(), eta.data(), stream);
       if (rc2 == TEM_ECUDA || rc2 == TEM_EINVAL) return rc2;
       if (rc2 != TEM_OK && rc_solve == TEM_OK) {
         rc_solve = rc2;
@@ -1299,16 +1306,23 @@ static int forward(tem_ctx* c, const double* mass, const double* f, int S, const
       TEM_CUDA(cudaGetLastError());
       std::vector<double> dst(4 * n);
       if (int rc = rows_to_host(c, part, 4 * n, L.nblk, dout, dst.data(), stream)) return rc;
-      if (int rc = resid_dd(c, mass, f, S, shifts, list, xc, r, L, w, res_now, stream)) return rc;
+      std::vector<double> abs_now;
+      if (int rc = resid_dd(c, mass, f, S, shifts, list, xc, r, L, w, res_now, stream, &abs_now)) return rc;
       // per shift: the contraction this round achieved, c_s = min(1, safety *
-      // ||r_s after|| / ||r_s before||) (the residual ratio times an
-      // allowance for the error-to-residual amplification), and the
-      // triangle-inequality size of its correction in each channel
+      // residual ratio) (an allowance for the error-to-residual
+      // amplification), and the triangle-inequality size of its correction
+      // in each channel
       std::vector<double> worst(S, 0.0), contr(S, 0.0);
       for (int y = 0; y < n; ++y) {
         const int s = list[y];
         const double rho_after = sqrt(res_now[y]);
-        contr[s] = std::min(1.0, o.safety * rho_after / std::max(res_prev[s], 1e-300));
+        // the part of ||r after|| explained by the rounding of x itself,
+        // 2^-52 || |A| |x| ||, carries no error in the directions the channels
+        // see (its preimage is the rounding of x); what the correction solve
+        // left beyond it is max(eta_s, (||r after|| - floor) / ||r before||)
+        const double floor_s = 0x1p-52 * sqrt(std::max(abs_now[y], 0.0));
+        const double ratio = std::max(eta[s], (rho_after - floor_s) / std::max(res_prev[s], 1e-300));
+        contr[s] = std::min(1.0, o.safety * ratio);
         const double wgt = is_pair[s] ? 2.0 : 1.0;
         for (int k = 0; k < K; ++k) {
           const double ar = residues[2 * ((size_t)k * S + s)], ai = residues[2 * ((size_t)k * S + s) + 1];
@@ -1344,12 +1358,12 @@ static int forward(tem_ctx* c, const double* mass, const double* f, int S, const
       // next round: every shift whose own correction could still matter
       // (triangle size above its share of the target), each asked for the
       // residual reduction that brings the estimate to half the target
-      const double eta = std::min(o.refine_tol, std::max(1e-9, 0.5 * o.channel_tol / (o.safety * bound)));
+      const double eta_next = std::min(o.refine_tol, std::max(1e-9, 0.5 * o.channel_tol / (o.safety * bound)));
       std::vector<int> next;
       for (int s : list)
         if (worst[s] * contr[s] > o.channel_tol / S) {
           next.push_back(s);
-          tols[s] = eta;
+          tols[s] = eta_next;
         }
       list = next;
       if (list.empty()) break;

@@ -79,6 +79,7 @@ struct ResidArgs {
   const double2* x;       // shift block
   double2* r;             // shift block (output; only the listed shifts are written)
   double* part;           // [nlist][gridDim.x]
+  double* part_abs;       // [nlist][gridDim.x]: || |A| |x| ||^2 partials (rounding floor), or NULL
   int list[32];
   double2 shifts[32];     // shift of list[y]
 };
@@ -90,7 +91,8 @@ __global__ void __launch_bounds__(256) k_resid_dd(const __grid_constant__ ResidA
   const double2* x = A.x + (long long)s * 3 * g.Nn;
   double2* r = A.r + (long long)s * 3 * g.Nn;
   const int nx1 = g.n[0] + 1, ny1 = g.n[1] + 1;
-  double acc = 0.0;
+  double acc = 0.0, acc_abs = 0.0;
+  auto ab = [](double2 v) { return fabs(v.x) + fabs(v.y); };
   for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < g.Nn;
        n += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(n % nx1);
@@ -148,6 +150,21 @@ __global__ void __launch_bounds__(256) k_resid_dd(const __grid_constant__ ResidA
       q[2] = cdd_sub(q[2], cdd_scale(circ4(Z(-1, 0, 0), X(-1, 0, 1), Z(0, 0, 0), X(-1, 0, 0)), wy_x));
       q[2] = cdd_add(q[2], cdd_scale(circ4(Y(0, -1, 0), Z(0, 0, 0), Y(0, -1, 1), Z(0, -1, 0)), wx_y));
     }
+    // (|K| |x|)_e with |x| taken as |Re| + |Im|: the scale of the rounding
+    // floor of the residual, eps || |A| |x| || (the residual of x rounded)
+    double qa[3] = {0.0, 0.0, 0.0};
+    if (A.part_abs) {
+      auto a4 = [&](double2 a, double2 b, double2 c, double2 d) { return ab(a) + ab(b) + ab(c) + ab(d); };
+      const double tz = wz * a4(X(0, 0, 0), Y(1, 0, 0), X(0, 1, 0), Y(0, 0, 0));
+      const double ty = wy * a4(Z(0, 0, 0), X(0, 0, 1), Z(1, 0, 0), X(0, 0, 0));
+      const double tx = wx * a4(Y(0, 0, 0), Z(0, 1, 0), Y(0, 0, 1), Z(0, 0, 0));
+      qa[0] = tz + ty + wz_y * a4(X(0, -1, 0), Y(1, -1, 0), X(0, 0, 0), Y(0, -1, 0)) +
+              wy_z * a4(Z(0, 0, -1), X(0, 0, 0), Z(1, 0, -1), X(0, 0, -1));
+      qa[1] = tz + tx + wz_x * a4(X(-1, 0, 0), Y(0, 0, 0), X(-1, 1, 0), Y(-1, 0, 0)) +
+              wx_z * a4(Y(0, 0, -1), Z(0, 1, -1), Y(0, 0, 0), Z(0, 0, -1));
+      qa[2] = ty + tx + wy_x * a4(Z(-1, 0, 0), X(-1, 0, 1), Z(0, 0, 0), X(-1, 0, 0)) +
+              wx_y * a4(Y(0, -1, 0), Z(0, 0, 0), Y(0, -1, 1), Z(0, -1, 0));
+    }
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const long long slot = c * g.Nn + n;
@@ -163,19 +180,28 @@ __global__ void __launch_bounds__(256) k_resid_dd(const __grid_constant__ ResidA
         const dd ri = dd_neg(dd_add(q[c].im, smi));
         out = make_double2(rr.hi + rr.lo, ri.hi + ri.lo);
         acc = fma(out.x, out.x, fma(out.y, out.y, acc));
+        const double ta = qa[c] + (fabs(sh.x) + fabs(sh.y)) * m * ab(xv);
+        acc_abs = fma(ta, ta, acc_abs);
       }
       r[slot] = out;
     }
   }
   // block sum, fixed order
-  __shared__ double red[8];
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __shared__ double red[2][8];
+  for (int o = 16; o > 0; o >>= 1) {
+    acc += __shfl_down_sync(0xffffffffu, acc, o);
+    acc_abs += __shfl_down_sync(0xffffffffu, acc_abs, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = acc;
+    red[1][threadIdx.x >> 5] = acc_abs;
+  }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 2) {
     double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-    A.part[(long long)y * gridDim.x + blockIdx.x] = t;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[threadIdx.x][w];
+    if (threadIdx.x == 0) A.part[(long long)y * gridDim.x + blockIdx.x] = t;
+    else if (A.part_abs) A.part_abs[(long long)y * gridDim.x + blockIdx.x] = t;
   }
 }
 

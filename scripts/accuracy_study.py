@@ -27,6 +27,9 @@ def conducting_mask(fw, wl):
 
 
 SETTINGS = [("default", dict(tol=1e-12, refine=True)),
+            ("t12x1", dict(tol=1e-12, refine=1)),
+            ("t11eta1e-4x1", dict(tol=1e-11, refine=1, refine_tol=1e-4)),
+            ("t10eta1e-5x1", dict(tol=1e-10, refine=1, refine_tol=1e-5)),
             ("t11", dict(tol=1e-11, refine=True)),
             ("t12eta1e-2", dict(tol=1e-12, refine=True, refine_tol=1e-2)),
             ("plain", dict(refine=False)),
