@@ -251,7 +251,7 @@ typedef struct {
   double relres_max;                   /* max_s final relative residual (double-double if refined) */
   long long kernel_launches;           /* kernels launched (solves, synthesis, refinement) */
 } tem_forward_stats;
-/* tol 1e-10, maxit 200000, max_refine 0, refine_tol 5e-4, channel_tol 1e-7, safety 1.5 */
+/* tol 1e-10, maxit 200000, max_refine 0, refine_tol 1e-4, channel_tol 1e-7, safety 1.5 */
 void tem_forward_default_opts(tem_forward_opts* opts);
 size_t tem_forward_workspace_bytes(const tem_ctx* ctx, int S, int K);
 /*   mass, f: device (tem_edge_mass; real edge vector); shifts, residues

@@ -1403,7 +1403,7 @@ void tem_forward_default_opts(tem_forward_opts* o) {
   o->tol = 1e-10;
   o->maxit = 200000;
   o->max_refine = 0;
-  o->refine_tol = 5e-4;
+  o->refine_tol = 1e-4;
   o->channel_tol = 1e-7;
   o->safety = 1.5;
 }

@@ -323,7 +323,7 @@ class TemForward:
         return out
 
     @staticmethod
-    def opts(tol: float = 1e-10, maxit: int = 200000, refine: bool | int = False, refine_tol: float = 5e-4,
+    def opts(tol: float = 1e-10, maxit: int = 200000, refine: bool | int = False, refine_tol: float = 1e-4,
              channel_tol: float = 1e-7, safety: float = 1.5) -> "_lib.ForwardOpts":
         """tem_forward_opts.  refine=True: up to 8 rounds of iterative
         refinement with the channel-aware stopping rule (R13); an
