@@ -433,21 +433,30 @@ def run_ours(args):
         "gpu_launches": launches,
     }
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.config, args.cpu_iters)
+        line["cpu_baseline"] = cpu_baseline(args.config, args.cpu_iters, args.poles)
     if ws > 1:
         dist.destroy_process_group()
     return line
 
 
-def cpu_baseline(config: str, iters: int):
-    """The oracle (oracle/cocg.py, as it stands) on the same workload:
-    CSR assembly untimed, then `iters` COCG iterations of the hardest
-    (smallest |s|) shift, timed.  Bounded sample, scaled to SUI/s."""
-    from oracle import cocg, yee
+def _oracle_table(config: str, poles: str):
+    """The family the GPU arm solves, as DATA: `--poles fit` -> the product's
+    fit committed by scripts/make_product_fit_tables.py
+    (data/rational/<config>_fit.json, checked against a fresh fit by
+    tests/test_product_fit.py); `--poles table` -> the oracle's table."""
     from paper_2506_11657_b200 import RationalTable  # table reading only
+    return RationalTable.load(f"{config}_fit" if poles == "fit" else config)
+
+
+def cpu_baseline(config: str, iters: int, poles: str = "fit"):
+    """The oracle (oracle/cocg.py, as it stands) on the same workload and the
+    same shifted systems: CSR assembly untimed, then `iters` COCG iterations
+    of the hardest (smallest |s|) shift, timed.  Bounded sample, scaled to
+    SUI/s."""
+    from oracle import cocg, yee
     from workloads import make_workload
     wl = make_workload(config)
-    table = RationalTable.load(config)
+    table = _oracle_table(config, poles)
     asm = yee.assemble(wl)
     s = table.shifts[np.argmin(np.abs(table.shifts))]
     t0 = time.perf_counter()
@@ -464,10 +473,9 @@ def run_reference(args):
     if rank != 0:
         return None
     from oracle import cocg, yee
-    from paper_2506_11657_b200 import RationalTable
     from workloads import make_workload
     wl = make_workload(args.config)
-    table = RationalTable.load(args.config)
+    table = _oracle_table(args.config, args.poles)
     asm = yee.assemble(wl)
     s = complex(table.shifts[np.argmin(np.abs(table.shifts))])
     for _ in range(args.warmup):
@@ -483,7 +491,10 @@ def run_reference(args):
             "unit": "shift-unknown-iterations/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
-            "data": "synthetic", "config": {"workload": args.config, "unknowns": asm.n},
+            "data": "synthetic",
+            "config": {"workload": args.config, "unknowns": asm.n, "shifts": table.n_shift,
+                       "real_shifts": int(np.sum(table.shifts.imag == 0)), "channels": int(table.residues.shape[1]),
+                       "poles": args.poles, "degree": int(2 * table.is_pair.sum() + (~table.is_pair).sum())},
             "cpu_baseline": {"value": v, "unit": "shift-unknown-iterations/s", "cores": 1,
                              "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "shift-unknown-iterations/s",

@@ -87,6 +87,14 @@ class RationalTable:
         residues = res.view(np.complex128).reshape(m, K)[:n].copy()
         return cls(shifts, residues, ip[:n].astype(bool), t, ue.value)
 
+    def to_json(self) -> dict:
+        """The table in the layout of data/rational/*.json (load() reads it)."""
+        def c(a):
+            return [[float(z.real), float(z.imag)] for z in np.asarray(a, dtype=np.complex128).ravel()]
+        return {"shifts": c(self.shifts), "residues": [c(r) for r in self.residues],
+                "is_pair": [bool(b) for b in self.is_pair], "times": [float(t) for t in self.times],
+                "uniform_error": None if self.uniform_error is None else float(self.uniform_error)}
+
     @classmethod
     def load(cls, name_or_path: str) -> "RationalTable":
         """Read data/rational/<name>.json (inputs computed once on the host

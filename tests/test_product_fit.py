@@ -114,3 +114,18 @@ def test_bench_family_pins(RationalTable):
     assert np.all(np.diff(r) / r[1:] > 1e-3)
     print(f"bench family: {tab.n_shift} systems, {real.size} real poles, uniform error "
           f"{tab.uniform_error:.2e}")
+
+
+def test_committed_product_fit_tables_match_a_fresh_fit(RationalTable):
+    """data/rational/<config>_fit.json (the family bench.py's oracle arm
+    reads, written by scripts/make_product_fit_tables.py) is exactly what
+    tem_fit_family returns now: the oracle arm and the GPU arm (`--poles
+    fit`, fitted at run time) solve the same shifted systems."""
+    from workloads import CONFIG_NAMES, make_workload
+    for name in CONFIG_NAMES:
+        wl = make_workload(name)
+        fresh = RationalTable.fit(wl.times, wl.n_poles)
+        stored = RationalTable.load(f"{name}_fit")
+        np.testing.assert_array_equal(stored.shifts, fresh.shifts)
+        np.testing.assert_array_equal(stored.residues, fresh.residues)
+        np.testing.assert_array_equal(stored.is_pair, fresh.is_pair)
