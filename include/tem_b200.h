@@ -219,6 +219,12 @@ int tem_residual(tem_ctx* ctx, const double* mass, const double* f, int S, const
  *   x_s <- COCG(f) to tol;  u = synthesis(x);  then per round, for the shifts
  *   still refined: r_s = f - (K + s M) x_s in double-double arithmetic,
  *   d_s = COCG(r_s) to refine_tol (relative to ||r_s||), x_s += d_s.
+ * Per-shift targets (split scheme): the first solve snapshots each shift's x
+ * when its residual first reaches 10 tol; the change of x_s from there to the
+ * end, scaled by the residual ratio and safety, estimates the error E_s left
+ * in x_s as max_k ||w_s Re(alpha_ks dx_s)||_M / ||u_k||_M.  Shift s is asked
+ * for the reduction channel_tol / (4 S E_s), at least refine_tol, and a shift
+ * whose target is >= 1/2 is not refined.
  * Channel-aware stopping: after a round, shift s's contraction is
  * c_s = min(1, safety * max(eta_s, (||r_s after|| - floor_s) / ||r_s before||))
  * -- eta_s the reduction its correction solve achieved, floor_s =

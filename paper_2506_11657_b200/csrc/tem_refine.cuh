@@ -327,6 +327,65 @@ __global__ void __launch_bounds__(256) k_dsynth_mnorm(long long nslots, const do
   }
 }
 
+// Per-shift refinement targets (reading R13): the change of x_s between a
+// snapshot taken when shift s first reached 10x its tolerance and the end of
+// the first solve, d_s = x_s - snap_s (complex layout), and its M-weighted
+// moments sum m (Re d)^2, sum m (Im d)^2, sum m Re d Im d -> part[(s*3+t)*gridDim.x + x].
+// mode[s]: 0 no snapshot (d_s = 0), 1 complex snapshot, 2 real-layout snapshot.
+struct SnapArgs {
+  Grid g;
+  const double* mass;
+  const double2* x;       // shift block, complex layout (after the solve's epilogue)
+  const double2* snap;    // shift block, per-shift layout of the solve (mode)
+  double2* d;             // shift block out
+  double* part;
+  int mode[32];
+};
+
+__global__ void __launch_bounds__(256) k_snap_delta(const __grid_constant__ SnapArgs A) {
+  const Grid& g = A.g;
+  const int s = blockIdx.y, mode = A.mode[s];
+  const long long n3 = 3 * g.Nn;
+  const double2* x = A.x + (long long)s * n3;
+  double2* d = A.d + (long long)s * n3;
+  const double2* sc = A.snap + (long long)s * n3;
+  const double* sr = reinterpret_cast<const double*>(sc);
+  const int nx1 = g.n[0] + 1;
+  double a0 = 0, a1 = 0, a2 = 0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n3; e += (long long)gridDim.x * blockDim.x) {
+    double2 v = czero();
+    if (mode) {
+      const double2 xv = x[e];
+      double2 sv;
+      if (mode == 1) {
+        sv = sc[e];
+      } else {
+        const long long c = e / g.Nn, node = e - c * g.Nn;
+        sv = make_double2(sr[c * g.NnP + (node / nx1) * g.px + node % nx1 + 1], 0.0);
+      }
+      v = csub(xv, sv);
+      const double m = __ldg(A.mass + e);
+      a0 = fma(m * v.x, v.x, a0);
+      a1 = fma(m * v.y, v.y, a1);
+      a2 = fma(m * v.x, v.y, a2);
+    }
+    d[e] = v;
+  }
+  __shared__ double red[3][8];
+  double v3[3] = {a0, a1, a2};
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    for (int o = 16; o > 0; o >>= 1) v3[t] += __shfl_down_sync(0xffffffffu, v3[t], o);
+    if ((threadIdx.x & 31) == 0) red[t][threadIdx.x >> 5] = v3[t];
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[threadIdx.x][w];
+    A.part[((long long)s * 3 + threadIdx.x) * gridDim.x + blockIdx.x] = t;
+  }
+}
+
 // out[row] = sum_b part[row * ncol + b], one warp per row, fixed order.
 __global__ void k_rows_sum(const double* __restrict__ part, int nrow, int ncol, double* out) {
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
