@@ -405,6 +405,16 @@ static int check_device(const tem_ctx* c) {
   return TEM_OK;
 }
 
+// The sweeps index a shift block with unsigned 32-bit element indices (the
+// shift's offset included; real shifts count 8-byte elements): S * 6 Nn must
+// stay below 2^32.  HBM is the tighter limit (S = 14: 51 M nodes here, 53 M
+// nodes of COCG state in 180 GB).
+static int check_index(const tem_ctx* c, int S) {
+  if ((unsigned long long)S * 6ULL * (unsigned long long)c->g.Nn >= (1ULL << 32))
+    return fail(TEM_EINVAL, "S * 6 * nodes must be below 2^32 (32-bit element indices of the sweeps)");
+  return TEM_OK;
+}
+
 // sweep geometry of one scheme: xy tiles x z-chunks x shift slots, for tile
 // height ty (tem::kTYTwoSweep or tem::kTYSplit).  The z-range is split until
 // the grid covers ~4 waves of resident CTAs, so that a few remaining
@@ -674,6 +684,7 @@ int tem_apply_shifted(tem_ctx* c, const double* mass, int S, const double* shift
   if (!c || !mass || !shifts || !x || !y) return fail(TEM_EINVAL, "tem_apply_shifted: null pointer");
   if (int rc = check_S(S)) return rc;
   if (int rc = check_device(c)) return rc;
+  if (int rc = check_index(c, S)) return rc;
   tem::SweepArgs A{};
   int grid = 0;
   sweep_geometry(c, S, S, A, &grid);
@@ -1071,6 +1082,7 @@ int tem_cocg_solve_rhs(tem_ctx* c, const double* mass, const double* rhs, int S,
     return fail(TEM_EINVAL, "tem_cocg_solve_rhs: null pointer");
   if (int rc = check_S(S)) return rc;
   if (int rc = check_device(c)) return rc;
+  if (int rc = check_index(c, S)) return rc;
   if (maxit < 1) return fail(TEM_EINVAL, "tem_cocg_solve_rhs: need maxit >= 1");
   for (int s = 0; s < S; ++s)
     if (!(tols[s] > 0.0)) return fail(TEM_EINVAL, "tem_cocg_solve_rhs: need tols[s] > 0");
@@ -1182,6 +1194,7 @@ int tem_synthesize(tem_ctx* c, int S, int K, const double* residues, const int* 
   if (!c || !residues || !is_pair || !x || !u) return fail(TEM_EINVAL, "tem_synthesize: null pointer");
   if (int rc = check_S(S)) return rc;
   if (int rc = check_device(c)) return rc;
+  if (int rc = check_index(c, S)) return rc;
   if (K < 1) return fail(TEM_EINVAL, "tem_synthesize: K must be >= 1");
   return synth(c, S, K, residues, is_pair, reinterpret_cast<const double2*>(x), u, (cudaStream_t)stream_);
 }
@@ -1512,6 +1525,7 @@ int tem_forward(tem_ctx* c, const double* mass, const double* f, int S, const do
     return fail(TEM_EINVAL, "tem_forward: null pointer");
   if (int rc = check_S(S)) return rc;
   if (int rc = check_device(c)) return rc;
+  if (int rc = check_index(c, S)) return rc;
   if (K < 1) return fail(TEM_EINVAL, "tem_forward: K must be >= 1");
   if (int rc = check_opts(opts)) return rc;
   const FwdLayout L = fwd_layout(c, S, K);
@@ -1525,6 +1539,7 @@ int tem_residual(tem_ctx* c, const double* mass, const double* f, int S, const d
   if (!c || !mass || !f || !shifts || !x || !r) return fail(TEM_EINVAL, "tem_residual: null pointer");
   if (int rc = check_S(S)) return rc;
   if (int rc = check_device(c)) return rc;
+  if (int rc = check_index(c, S)) return rc;
   if (x == r) return fail(TEM_EINVAL, "tem_residual: x and r must not alias");
   cudaStream_t stream = (cudaStream_t)stream_;
   const int nblk = 2 * std::max(1, c->num_sms);
@@ -1573,6 +1588,7 @@ int tem_forward_host(tem_ctx* c, const double* sigma, const double* f, int S, co
     return fail(TEM_EINVAL, "tem_forward_host: null pointer");
   if (int rc = check_S(S)) return rc;
   if (int rc = check_device(c)) return rc;
+  if (int rc = check_index(c, S)) return rc;
   if (K < 1) return fail(TEM_EINVAL, "tem_forward_host: K must be >= 1");
   if (int rc = check_opts(opts)) return rc;
   const size_t ncell = (size_t)c->g.n[0] * c->g.n[1] * c->g.n[2];

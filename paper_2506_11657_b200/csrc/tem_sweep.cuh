@@ -154,6 +154,23 @@ __device__ __forceinline__ void tma_tile(void* dst, const CUtensorMap* tm, int c
       : "memory");
 }
 
+// Per-edge mass loads (8 B per edge, shared by the S shift CTAs of a tile):
+// they carry an L2 evict_last policy, so the streamed vectors do not push the
+// mass out between the shift slots of a band (measured on `large`: pass 1
+// even -0.6 GB of DRAM reads and -3.4% time, odd -1.7%).  The same policy in
+// reverse (evict_first) on the TMA loads breaks the halo reuse between
+// neighbouring tiles (+25% reads) and is not used.
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ double ld_mass(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 // Result stores of the sweeps are read again only by the next kernel (after
 // the whole vector has streamed through L2): streaming, evict-first, so they
 // do not displace the plane tiles and halo rows still to be re-read
@@ -170,16 +187,6 @@ __device__ __forceinline__ int pmod(int q, int n) { return (int)((unsigned)(q + 
 __device__ __forceinline__ double2* smem_align128(unsigned char* raw) {
   const uint32_t a = smem_u32(raw);
   return reinterpret_cast<double2*>(raw + ((128u - (a & 127u)) & 127u));
-}
-
-__device__ __forceinline__ bool free_x(const Grid& g, int i, int j, int k) {
-  return i < g.n[0] && j >= 1 && j <= g.n[1] - 1 && k >= 1 && k <= g.n[2] - 1;
-}
-__device__ __forceinline__ bool free_y(const Grid& g, int i, int j, int k) {
-  return i >= 1 && i <= g.n[0] - 1 && j < g.n[1] && k >= 1 && k <= g.n[2] - 1;
-}
-__device__ __forceinline__ bool free_z(const Grid& g, int i, int j, int k) {
-  return i >= 1 && i <= g.n[0] - 1 && j >= 1 && j <= g.n[1] - 1 && k < g.n[2];
 }
 
 // Block-wide sum of a complex and a real value (all NTH threads participate);
@@ -235,6 +242,11 @@ struct Column {
   double pxy, pxym, pxmy;   // ih_x ih_y, ih_x ih_y(j-1), ih_x(i-1) ih_y
   double cyx, cyxm;         // hd_y ih_x, hd_y ih_x(i-1)
   double cxy, cxym;         // hd_x ih_y, hd_x ih_y(j-1)
+  // bit c: edge c of the column is free (not on the boundary n x e = 0, eq:bc)
+  // as far as (i, j) decide: x: i < nx, 1 <= j <= ny-1; y: 1 <= i <= nx-1, j < ny;
+  // z: 1 <= i <= nx-1, 1 <= j <= ny-1.  The k part (x, y: 1 <= k <= nz-1;
+  // z: 0 <= k < nz) is per plane (stencil3p).
+  unsigned fm;
 };
 
 // Column constants of node column (i, j); i, j may lie outside the grid
@@ -259,6 +271,8 @@ __device__ __forceinline__ Column make_column_ij(const Grid& g, int i, int j) {
   C.cyxm = hdy * ihxm;
   C.cxy = hdx * ihy;
   C.cxym = hdx * ihym;
+  const bool ii = i >= 1 && i <= g.n[0] - 1, jj = j >= 1 && j <= g.n[1] - 1;
+  C.fm = !C.in_ij ? 0u : ((jj ? 1u : 0u) | (ii ? 2u : 0u) | (ii && jj ? 4u : 0u));
   return C;
 }
 
@@ -290,9 +304,12 @@ __device__ __forceinline__ void stencil3p(const Grid& g, const Column& C, int c0
                                           double ihzm, double hdz, const V* Xm, const V* X0, const V* Xp,
                                           const V* Ym, const V* Y0, const V* Yp, const V* Zm, const V* Z0,
                                           Edge3<V>& E) {
-  E.f[0] = C.in_ij && free_x(g, C.i, C.j, k);
-  E.f[1] = C.in_ij && free_y(g, C.i, C.j, k);
-  E.f[2] = C.in_ij && k >= 0 && free_z(g, C.i, C.j, k);
+  {   // free edges: the (i, j) part is per column (Column::fm), only the k part changes per plane
+    const bool kxy = k >= 1 && k <= g.n[2] - 1, kz = k >= 0 && k < g.n[2];
+    E.f[0] = kxy && (C.fm & 1u);
+    E.f[1] = kxy && (C.fm & 2u);
+    E.f[2] = kz && (C.fm & 4u);
+  }
 #define T_(P, di, dj) P[c0 + (dj) * PITCH + (di)]
   const V x00 = T_(X0, 0, 0), y00 = T_(Y0, 0, 0), z00 = T_(Z0, 0, 0);
   // face weights W = hdual / (mu0 A)
@@ -635,14 +652,21 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
   }
 
   const Column C = make_column<TYV>(g, tx0, ty0);
-  const long long cst = vcomp<V>(g);                 // component stride of this layout
+  // element indices inside one shift's vector are 32-bit (3 NnP < 2^31), and
+  // with the shift's offset unsigned 32-bit (check_index in tem_b200.cu): an
+  // address is a kernel-parameter base + one widening multiply-add instead of
+  // a 64-bit index chain per access (-8..-15% instructions in the split pass 1)
+  typedef int idx_t;
+  const idx_t cst = (idx_t)vcomp<V>(g);              // component stride of this layout
   const int rowp = vrow<V>(g);                       // node row pitch of this layout
   const int nx1 = g.n[0] + 1, ny1 = g.n[1] + 1;
-  V* out = vbase<V>(B.out, s, g);
-  V* xv = vbase<V>(A.x, s, g);
-  V* zv = vbase<V>(B.z, s, g);
-  const V* zin = vbase<V>(B.zin, s, g);
-  const V* pold = vbase<V>(B.pold, s, g);
+  const unsigned sb = (unsigned)s * (unsigned)((VT<V>::kReal ? 6 : 3) * g.Nn);   // the shift's offset
+  V* out = reinterpret_cast<V*>(B.out);
+  V* xv = reinterpret_cast<V*>(A.x);
+  V* zv = reinterpret_cast<V*>(B.z);
+  const V* zin = reinterpret_cast<const V*>(B.zin);
+  const V* pold = reinterpret_cast<const V*>(B.pold);
+#define TEM_EI(e) ((unsigned)(e) + sb)
   for (int q = tid; q <= ke - kb; q += NT) {
     const int k = kb - 1 + q;
     zih[q] = k >= 0 ? __ldg(g.ih[2] + k) : 0.0;
@@ -719,21 +743,24 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
   // centre operands (mass; MODE 2: x, z; MODE 4: x, z) of the next step, loaded a step ahead
   double mN[3];
   V xN[3], zN[3];
-  auto load_centre = [&](int k) {
-    const long long node = ((long long)k * ny1 + C.j) * nx1 + C.i;
-    const long long nodeV = ((long long)k * ny1 + C.j) * rowp + C.i + vofs<V>();
-    const bool ok = C.in_ij && k < g.n[2];
+  const uint64_t mass_pol = l2_policy_evict_last();
+  // threads outside the grid (partial tiles) load column (0, 0): valid memory,
+  // values unused (none of their edges is free) -- no predicates, no zero fill
+  const int ci = C.in_ij ? C.i : 0, cj = C.in_ij ? C.j : 0;
+  auto load_centre = [&](int k) {   // kb <= k < ke <= nz
+    const idx_t node = ((idx_t)k * ny1 + cj) * nx1 + ci;
+    const idx_t nodeV = ((idx_t)k * ny1 + cj) * rowp + ci + vofs<V>();
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      mN[c] = ok ? __ldg(A.mass + c * g.Nn + node) : 0.0;
-      const long long slot = c * cst + nodeV;
+      mN[c] = ld_mass(A.mass + (unsigned)(c * (idx_t)g.Nn + node), mass_pol);
+      const idx_t slot = c * cst + nodeV;
       if (MODE == 2) {
-        xN[c] = ok ? xv[slot] : VT<V>::zero();
-        zN[c] = ok ? zv[slot] : VT<V>::zero();
+        xN[c] = xv[TEM_EI(slot)];
+        zN[c] = zv[TEM_EI(slot)];
       }
       if (MODE == 4) {
-        xN[c] = ok ? __ldcg(xv + slot) : VT<V>::zero();
-        zN[c] = ok ? __ldcg(zin + slot) : VT<V>::zero();
+        xN[c] = __ldcg(xv + TEM_EI(slot));
+        zN[c] = __ldcg(zin + TEM_EI(slot));
       }
     }
   };
@@ -743,8 +770,8 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
   // k-2, k-1, k), Z of k-1, k (sets k-1, k); rotated once per step
   int sxm = pmod(kb - 2, R_XY), sx0 = pmod(kb - 1, R_XY), sxp = pmod(kb, R_XY);
   int szm = pmod(kb - 1, R_Z), sz0 = pmod(kb, R_Z);
-  const long long col = (long long)C.j * rowp + C.i + vofs<V>();   // own column, component 0, plane 0
-  const long long plane = (long long)rowp * ny1;
+  const idx_t col = (idx_t)C.j * rowp + C.i + vofs<V>();   // own column, component 0, plane 0
+  const idx_t plane = (idx_t)rowp * ny1;
 #pragma unroll 1
   for (int k = kb; k < ke; ++k) {
     if (!kZ) wait_set(k);
@@ -757,7 +784,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
     sxp = sxp + 1 == R_XY ? 0 : sxp + 1;
     szm = sz0;
     sz0 = sz0 + 1 == R_Z ? 0 : sz0 + 1;
-    const long long ek = col + (long long)k * plane;
+    const idx_t ek = col + (idx_t)k * plane;
     if (kZOwn) {   // own z_i from the staging tiles: X, Y of set k-1, Z of set k
       const V* zk1 = zs + pmod(k - 1, RS) * 3 * TSV;
       const V* zk = zs + pmod(k, RS) * 3 * TSV;
@@ -768,7 +795,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       if (!E.f[c]) continue;
-      const long long e = ek + c * cst;
+      const auto e = TEM_EI(ek + c * cst);
       const V q = cfma(sh, cscale(mN[c], E.p[c]), E.q[c]);   // (K + s M) v
       if (kUpd) {
         const V D = VT<V>::make(E.kd[c] + mN[c] * sh2.x, mN[c] * sh2.y);
@@ -819,6 +846,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
   P.m = VT<V>::cplx(acc_m);
   P.q = VT<V>::cplx(acc_q);
   P.r = acc_r;
+#undef TEM_EI
 }
 
 // Split pass 1: the CTA's partial sums (gamma, eps, mu, ||r||^2, s z^T M z)
