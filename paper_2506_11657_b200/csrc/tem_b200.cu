@@ -372,7 +372,7 @@ struct tem_ctx {
   int launch_mode = TEM_LAUNCH_AUTO;
   int solver = TEM_SOLVER_SPLIT;
   int band = 4;                     // tile rows per band of the block order (block_coords), 32x8 tiles
-  int band_split = 8;               // the same for the split scheme's 32x12 tiles (measured best)
+  int band_split = 96 / tem::kTYSplit;   // the same for the split scheme's 32x12 tiles: 8 (measured best)
   int real_arith = 1;               // real shifts in real arithmetic (split scheme; TEM_NO_REAL=1 disables)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;   // loop timing of the last solve
   int last_persistent = 0;          // the last solve ran k_persist

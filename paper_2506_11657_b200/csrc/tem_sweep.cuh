@@ -54,11 +54,17 @@ struct Tile {
   static constexpr int TS2 = TILE_STRIDE / 16;     // slot pitch in double2
   static constexpr size_t kSmemDirect = 128 + (size_t)(2 * R_XY + R_Z) * TILE_STRIDE;
   static constexpr size_t kSmemDirap = kSmemDirect + (size_t)6 * TILE_STRIDE;    // + z staging, 2 sets
-  static constexpr size_t kSmemUpd = kSmemDirect + (size_t)12 * TILE_STRIDE;     // + z staging, 4 sets
+  // even split pass: 4 staged z sets (own z_i served from them); a tile lower than 12 rows runs
+  // 2 CTAs per SM and has room for 2 sets only (own z_i re-read)
+  static constexpr int kStageSets = TYV >= 12 ? 4 : 2;
+  static constexpr size_t kSmemUpd = kSmemDirect + (size_t)3 * kStageSets * TILE_STRIDE;
   static constexpr size_t kSmemDelta = 128 + (size_t)3 * R_D * TILE_STRIDE;
 };
 constexpr int kTYTwoSweep = 8;    // tile height of MODE 0, 1, 2
-constexpr int kTYSplit = 12;      // tile height of MODE 3, 4 and k_delta
+#ifndef TEM_TY_SPLIT
+#define TEM_TY_SPLIT 12           // build-variant experiments: -DTEM_TY_SPLIT=6 (192 threads, 2 CTAs per SM)
+#endif
+constexpr int kTYSplit = TEM_TY_SPLIT;   // tile height of MODE 3, 4 and k_delta
 #define TEM_TILE_CONSTANTS(TYV)                                                              \
   constexpr int TX = Tile<TYV>::TX, TY = Tile<TYV>::TY, NT = Tile<TYV>::NT;                 \
   constexpr int HX = Tile<TYV>::HX, HY = Tile<TYV>::HY, TS2 = Tile<TYV>::TS2;               \
@@ -629,7 +635,8 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
   V* rZ = ring + 2 * R_XY * TSV;       // [R_Z]
   // z staging [RS][3 tiles]: 2 sets (MODE 1, 4); 4 sets (MODE 3), so that the
   // node's own z_i (X, Y of set k-1, Z of set k) is still staged at step k
-  constexpr bool kZOwn = (MODE == 3);   // own z_i from staging (MODE 4: re-read, fewer registers)
+  // own z_i from the staging (else re-read from global memory)
+  constexpr bool kZOwn = MODE == 3 && Tile<TYV>::kStageSets == 4;
   constexpr int RS = kZOwn ? 4 : 2;
   V* zs = ring + (2 * R_XY + R_Z) * TSV;
   const Grid& g = A.g;
@@ -758,10 +765,8 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
         xN[c] = xv[TEM_EI(slot)];
         zN[c] = zv[TEM_EI(slot)];
       }
-      if (MODE == 4) {
-        xN[c] = __ldcg(xv + TEM_EI(slot));
-        zN[c] = __ldcg(zin + TEM_EI(slot));
-      }
+      if (MODE == 4) xN[c] = __ldcg(xv + TEM_EI(slot));
+      if (kUpd && !kZOwn) zN[c] = __ldcg(zin + TEM_EI(slot));
     }
   };
   load_centre(kb);
