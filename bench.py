@@ -376,8 +376,10 @@ def run_ours(args):
     if os.path.exists(tpath):
         try:
             tj = json.load(open(tpath)).get(solver, {})
-            traffic = tj.get("traffic_bytes_per_iteration")
-            traffic_alg = tj.get("algorithmic_bytes_per_iteration")
+            # the capture is of one workload and family; other runs report no traffic
+            if tj.get("workload", "large") == args.config and tj.get("poles", "fit") == args.poles:
+                traffic = tj.get("traffic_bytes_per_iteration")
+                traffic_alg = tj.get("algorithmic_bytes_per_iteration")
         except Exception:
             traffic = None
     n_real = int(np.sum(table.shifts.imag == 0)) if (real_arith and solver == "split") else 0

@@ -13,6 +13,7 @@ serialised: compare shares, not absolutes).
 import collections
 import csv
 import json
+import os
 import subprocess
 import sys
 
@@ -82,5 +83,42 @@ def full(src, dst):
             print(f"  {k}: {v}")
 
 
+def _bytes(v):
+    x, unit = v.split()
+    return float(x) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}[unit]
+
+
+def traffic(src, dst):
+    """profiles/traffic.json `split` entry from a `full` summary of the split
+    passes on the bench workload (`large`, library poles: 10 complex + 4 real
+    shifts, all active): DRAM bytes per COCG iteration = mean of an even and an
+    odd pass 1 plus pass 2, against the algorithmic bytes."""
+    recs = json.load(open(src))
+    per = {}
+    for r in recs:
+        name = r["Kernel Name"].split("(")[0].replace("void ", "").replace("tem::", "")
+        name = name.replace("(int)", "").replace("(bool)", "")
+        per.setdefault(name, []).append(_bytes(r["dram__bytes_read.sum"]) + _bytes(r["dram__bytes_write.sum"]))
+    per = {k: sum(v) / len(v) for k, v in per.items()}
+    ev = next(v for k, v in per.items() if k.startswith("k_sweep<3"))
+    od = next(v for k, v in per.items() if k.startswith("k_sweep<4"))
+    de = next(v for k, v in per.items() if k.startswith("k_delta"))
+    n_unknowns, n_complex, n_real = 13984256, 10, 4
+    alg = 96.0 * n_unknowns * n_complex + 48.0 * n_unknowns * n_real
+    out = json.load(open(dst)) if os.path.exists(dst) else {}
+    out["split"] = {
+        "source": src + " (ncu --set full, `large`, library poles: 10 complex + 4 real shifts, all active)",
+        "workload": "large", "poles": "fit",
+        "traffic_bytes_per_iteration": 0.5 * (ev + od) + de,
+        "algorithmic_bytes_per_iteration": alg,
+        "bytes_per_complex_sui": (0.5 * (ev + od) + de) / (n_unknowns * (n_complex + 0.5 * n_real)),
+        "algorithmic_bytes_per_complex_sui": 96.0,
+        "per_kernel_bytes": per,
+        "iteration": "mean of an even (k_sweep<3,12>) and an odd (k_sweep<4,12>) pass 1, plus k_delta",
+    }
+    json.dump(out, open(dst, "w"), indent=1)
+    print(json.dumps(out["split"], indent=1))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](sys.argv[2], sys.argv[3])

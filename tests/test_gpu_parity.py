@@ -217,6 +217,28 @@ def test_edge_cases(solver):
     assert d < 1e-6
 
 
+def test_index_range_rejected_before_launch():
+    """The sweeps use unsigned 32-bit element indices: a grid with
+    S * 6 * nodes >= 2^32 is refused (TEM_EINVAL) before any launch."""
+    import ctypes
+    lib = _lib.load()
+    nx, ny, nz = 330, 330, 220            # 24.2 M nodes: 32 * 6 * Nn > 2^32, 8 * 6 * Nn < 2^32
+    h = ctypes.c_void_p()
+    w = np.ones(nx)
+    dp = w.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    with torch.cuda.device(0):
+        assert lib.tem_create(nx, ny, nz, dp, dp, dp, ctypes.byref(h)) == 0
+        try:
+            dummy = torch.zeros(8, dtype=torch.float64, device="cuda")
+            ptr = ctypes.c_void_p(dummy.data_ptr())
+            sh = np.ones(64)
+            rc = lib.tem_apply_shifted(h, ptr, 32, sh.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ptr, ptr, None)
+            assert rc == -1                                   # TEM_EINVAL
+            assert b"2^32" in lib.tem_last_error()
+        finally:
+            lib.tem_destroy(h)
+
+
 def test_forward_host_matches_device_path():
     wl = make_workload("tiny")
     fw, asm, slots, table, sigma, f = _setup(wl)
