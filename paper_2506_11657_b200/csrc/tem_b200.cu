@@ -154,6 +154,46 @@ __device__ __forceinline__ void init_body(const tem::SweepArgs& A, int s, int b,
   zmz2 = tem::VT<V>::cplx(zmz);
 }
 
+// The same for a pair of real shifts (leader s, partner sp): the packed
+// vectors (component x: s, component y: sp) go to the leader's block in the
+// complex layout; rr2 is ||b||^2 of the partner.
+__device__ __forceinline__ void init_pair(const tem::SweepArgs& A, int s, int sp, int b, int nb, double2* p0,
+                                          double2* p1, double2* z1, const double* __restrict__ f, double2& rho2,
+                                          double& rr, double& rr2, double2& zmz2) {
+  const Grid& g = A.g;
+  const double sa = A.st[s].s.x, sb = A.st[sp].s.x;
+  const long long off = (long long)s * 3 * g.Nn;
+  const double2* ra = A.rhs ? A.rhs + off : nullptr;
+  const double2* rb = A.rhs ? A.rhs + (long long)sp * 3 * g.Nn : nullptr;
+  double2 rho = tem::czero(), zmz = tem::czero();
+  for (long long slot = b * 256LL + threadIdx.x; slot < 3 * g.Nn; slot += (long long)nb * 256) {
+    double2 z = tem::czero();
+    const double m = __ldg(A.mass + slot);
+    if (m > 0.0) {
+      const int a = (int)(slot / g.Nn);
+      int pos[3];
+      tem::node_pos(g, slot - a * g.Nn, pos);
+      const double kd = kdiag(g, a, pos);
+      const double fa = ra ? __ldg(&ra[slot].x) : __ldg(f + slot);
+      const double fb = rb ? __ldg(&rb[slot].x) : __ldg(f + slot);
+      z = make_double2(fa / fma(m, sa, kd), fb / fma(m, sb, kd));
+      rho.x = fma(fa, z.x, rho.x);
+      rho.y = fma(fb, z.y, rho.y);
+      rr = fma(fa, fa, rr);
+      rr2 = fma(fb, fb, rr2);
+      zmz.x = fma(m, z.x * z.x, zmz.x);
+      zmz.y = fma(m, z.y * z.y, zmz.y);
+    }
+    A.x[off + slot] = tem::czero();
+    A.z[off + slot] = z;
+    p0[off + slot] = tem::czero();
+    p1[off + slot] = tem::czero();
+    if (z1) z1[off + slot] = tem::czero();
+  }
+  rho2 = rho;
+  zmz2 = zmz;
+}
+
 __global__ void __launch_bounds__(256) k_init(tem::SweepArgs A, double2* p0, double2* p1, double2* z1,
                                               const double* __restrict__ f) {
   __shared__ double red[3 * 8];
@@ -162,37 +202,54 @@ __global__ void __launch_bounds__(256) k_init(tem::SweepArgs A, double2* p0, dou
   const int nb = gridDim.x / S;
   const int b = blockIdx.x / S;
   double2 rho = tem::czero(), zmz = tem::czero();
-  double rr = 0.0;
-  if (A.st[s].real)
+  double rr = 0.0, rr2 = 0.0;
+  const int partner = A.st[s].pair - 1;
+  if (partner >= 0) {   // the leader's blocks initialise the pair; the partner's blocks have nothing to do
+    if (A.st[s].lead) init_pair(A, s, partner, b, nb, p0, p1, z1, f, rho, rr, rr2, zmz);
+  } else if (A.st[s].real) {
     init_body<double>(A, s, b, nb, p0, p1, z1, f, rho, rr, zmz);
-  else
+  } else {
     init_body<double2>(A, s, b, nb, p0, p1, z1, f, rho, rr, zmz);
+  }
   tem::block_sum_n<256>(rho, rr, red);
-  double dum = 0.0;
-  tem::block_sum_n<256>(zmz, dum, red);
+  tem::block_sum_n<256>(zmz, rr2, red);
   if (threadIdx.x == 0) {
     A.part_c[blockIdx.x] = rho;
     A.part_r[blockIdx.x] = rr;
     A.part[9 * A.pstride + blockIdx.x] = zmz.x;
     A.part[10 * A.pstride + blockIdx.x] = zmz.y;
+    A.part[11 * A.pstride + blockIdx.x] = rr2;
   }
   if (!tem::last_block(&A.ctl->ticket[0])) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int q = warp; q < S; q += 8) {
-    double cx = 0, cy = 0, cr = 0, mx = 0, my = 0;
-    for (int bb = q + lane * S; bb < (int)gridDim.x; bb += 32 * S) {
+    // the sums of a pair live in its leader's blocks: (x, rr) the leader's, (y, rr2) the partner's
+    const int qp = A.st[q].pair - 1;
+    const bool second = qp >= 0 && !A.st[q].lead;
+    const int src = second ? qp : q;
+    double cx = 0, cy = 0, cr = 0, mx = 0, my = 0, cr2 = 0;
+    for (int bb = src + lane * S; bb < (int)gridDim.x; bb += 32 * S) {
       const double2 v = __ldcg(A.part_c + bb);
       cx += v.x;
       cy += v.y;
       cr += __ldcg(A.part_r + bb);
       mx += __ldcg(A.part + 9 * A.pstride + bb);
       my += __ldcg(A.part + 10 * A.pstride + bb);
+      cr2 += __ldcg(A.part + 11 * A.pstride + bb);
     }
     cx = tem::warp_sum(cx);
     cy = tem::warp_sum(cy);
     cr = tem::warp_sum(cr);
     mx = tem::warp_sum(mx);
     my = tem::warp_sum(my);
+    cr2 = tem::warp_sum(cr2);
+    if (qp >= 0) {   // real sums of this member
+      cx = second ? cy : cx;
+      mx = second ? my : mx;
+      cr = second ? cr2 : cr;
+      cy = 0.0;
+      my = 0.0;
+    }
     if (lane == 0) {
       tem::ShiftState& st = A.st[q];
       st.rho = make_double2(cx, cy);
@@ -207,12 +264,36 @@ __global__ void __launch_bounds__(256) k_init(tem::SweepArgs A, double2* p0, dou
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int na = 0;
-    for (int q = 0; q < S; ++q)
-      if (A.st[q].active) A.ctl->list[na++] = q;
-    A.ctl->n_active = na;
-    A.ctl->ticket[0] = 0;
+  if (threadIdx.x < 32) {
+    __threadfence();
+    tem::rebuild_list(A);
+    if (threadIdx.x == 0) A.ctl->ticket[0] = 0;
+  }
+}
+
+// Pairing (R16): real shifts with real right-hand sides (ShiftState::real,
+// final after k_real_mask) are sorted by shift -- iteration counts grow as s
+// falls, so neighbours stop at about the same time -- and paired two by two;
+// an odd one out stays a single real shift.  One thread; S <= 32.
+__global__ void k_pair(tem::ShiftState* st, int S, int enable) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int idx[TEM_MAX_SHIFTS], n = 0;
+  for (int s = 0; s < S; ++s) {
+    st[s].pair = 0;
+    st[s].lead = 0;
+    if (enable && st[s].real) idx[n++] = s;
+  }
+  for (int i = 1; i < n; ++i)   // insertion sort, descending shift
+    for (int j = i; j > 0 && st[idx[j]].s.x > st[idx[j - 1]].s.x; --j) {
+      const int t = idx[j];
+      idx[j] = idx[j - 1];
+      idx[j - 1] = t;
+    }
+  for (int i = 0; i + 1 < n; i += 2) {
+    st[idx[i]].pair = idx[i + 1] + 1;
+    st[idx[i]].lead = 1;
+    st[idx[i + 1]].pair = idx[i] + 1;
+    st[idx[i + 1]].lead = 0;
   }
 }
 
@@ -246,6 +327,22 @@ __global__ void __launch_bounds__(256) k_xfix(tem::SweepArgs A, const double2* _
   const int S = A.S;
   const int s = blockIdx.x % S;
   const tem::ShiftState& st = A.st[s];
+  if (st.pair) {
+    // a pair ran max(iters) iterations; if the last one was even, each member's
+    // pending step length is its alpha_prev (0 if it was frozen earlier, R16)
+    if (!st.lead) return;
+    const tem::ShiftState& sp = A.st[st.pair - 1];
+    if ((max(st.iters, sp.iters) & 1) == 0) return;
+    const double ax = st.alpha_prev.x, ay = sp.alpha_prev.x;
+    double2* x = A.x + (long long)s * 3 * A.g.Nn;
+    const double2* p = p1 + (long long)s * 3 * A.g.Nn;
+    const int b = blockIdx.x / S, nb = gridDim.x / S;
+    for (long long slot = b * 256LL + threadIdx.x; slot < 3 * A.g.Nn; slot += (long long)nb * 256) {
+      const double2 pv = p[slot], xv = x[slot];
+      x[slot] = make_double2(fma(ax, pv.x, xv.x), fma(ay, pv.y, xv.y));
+    }
+    return;
+  }
   if ((st.iters & 1) == 0) return;
   const double2 a = st.active ? st.alpha_prev : st.alpha;
   if (st.real)
@@ -258,10 +355,26 @@ __global__ void __launch_bounds__(256) k_xfix(tem::SweepArgs A, const double2* _
 // Pass 0 copies the real vector to tmp (the same shift's region of a free
 // work vector); pass 1 expands tmp into x (imaginary parts 0, non-free and
 // non-existent slots 0).
+// A pair's packed x (leader's block) -> the two members' blocks in the ABI
+// layout (real parts, imaginary parts 0); element-wise, in place.
+__global__ void __launch_bounds__(256) k_pair_out(tem::SweepArgs A) {
+  const int S = A.S;
+  const int s = blockIdx.x % S;
+  if (!A.st[s].pair || !A.st[s].lead) return;
+  const int b = blockIdx.x / S, nb = gridDim.x / S;
+  double2* xa = A.x + (long long)s * 3 * A.g.Nn;
+  double2* xb = A.x + (long long)(A.st[s].pair - 1) * 3 * A.g.Nn;
+  for (long long slot = b * 256LL + threadIdx.x; slot < 3 * A.g.Nn; slot += (long long)nb * 256) {
+    const double2 v = xa[slot];
+    xa[slot] = make_double2(v.x, 0.0);
+    xb[slot] = make_double2(v.y, 0.0);
+  }
+}
+
 __global__ void __launch_bounds__(256) k_real_out(tem::SweepArgs A, double2* tmp, int pass) {
   const int S = A.S;
   const int s = blockIdx.x % S;
-  if (!A.st[s].real) return;
+  if (!A.st[s].real || A.st[s].pair) return;
   const int b = blockIdx.x / S, nb = gridDim.x / S;
   const Grid& g = A.g;
   const double* xr = tem::vbase<double>(A.x, s, g);
@@ -933,6 +1046,11 @@ static int solve(tem_ctx* c, const double* mass, const double* f, const double2*
     TEM_CUDA(cudaGetLastError());
     launches += 2;
   }
+  // pairs of real shifts share a slot (R16); the persistent path runs them singly
+  const bool persistent = split && use_persistent(c, S);
+  const int pairing = split && c->real_arith && any_real && !persistent && !getenv("TEM_NO_PAIR");
+  k_pair<<<1, 32, 0, stream>>>(base.st, S, pairing);
+  launches += 1;
   const bool dbg = getenv("TEM_DEBUG_SYNC") != nullptr;   // debugging: locate a failing launch
 #define TEM_DBG(name)                                                                               \
   if (dbg) {                                                                                        \
@@ -956,7 +1074,7 @@ static int solve(tem_ctx* c, const double* mass, const double* f, const double2*
   const bool trace = getenv("TEM_TRACE") != nullptr;
   auto t_prev = std::chrono::steady_clock::now();
   int done = 0;
-  c->last_persistent = split && use_persistent(c, S) ? 1 : 0;
+  c->last_persistent = persistent ? 1 : 0;
   if (c->last_persistent) {
     // one cooperative launch runs up to kPersistIters iterations; z-chunking
     // per active-slot count for one resident CTA per SM (latency regime)
@@ -1030,9 +1148,11 @@ static int solve(tem_ctx* c, const double* mass, const double* f, const double2*
       snap_pending = false;
       for (int s = 0; s < S; ++s) {
         if (!snap->mode[s] && hs[s].active && hs[s].relres <= snap->tol) {
+          // a pair's x is packed in its leader's block (component x: leader, y: partner)
+          const int src = hs[s].pair && !hs[s].lead ? hs[s].pair - 1 : s;
           TEM_CUDA(cudaMemcpyAsync(snap->buf + (size_t)s * 3 * c->g.Nn, reinterpret_cast<double2*>(x) +
-                                   (size_t)s * 3 * c->g.Nn, vb, cudaMemcpyDeviceToDevice, stream));
-          snap->mode[s] = hs[s].real ? 2 : 1;
+                                   (size_t)src * 3 * c->g.Nn, vb, cudaMemcpyDeviceToDevice, stream));
+          snap->mode[s] = hs[s].pair ? (hs[s].lead ? 3 : 4) : hs[s].real ? 2 : 1;
           snap->relres[s] = hs[s].relres;
         }
         snap_pending |= !snap->mode[s] && hs[s].active;   // still to be taken
@@ -1049,7 +1169,11 @@ static int solve(tem_ctx* c, const double* mass, const double* f, const double2*
     k_xfix<<<vec_grid, 256, 0, stream>>>(base, P[1]);
     launches += 1;
     TEM_DBG("k_xfix");
-    if (any_real) {   // real-layout x of real shifts -> complex ABI layout (Z[0] as scratch)
+    if (any_real) {   // real-layout / pair-packed x of real shifts -> complex ABI layout (Z[0] as scratch)
+      if (pairing) {
+        k_pair_out<<<vec_grid, 256, 0, stream>>>(base);
+        launches += 1;
+      }
       k_real_out<<<vec_grid, 256, 0, stream>>>(base, Z[0], 0);
       k_real_out<<<vec_grid, 256, 0, stream>>>(base, Z[0], 1);
       launches += 2;

@@ -92,17 +92,66 @@ __device__ __forceinline__ double crcp(double b, double& n) {
   return fma(r, fma(-b, r, 1.0), r);
 }
 
+// Two real shifts in one complex-sized slot (R16): the systems
+// K + s_A M and K + s_B M of two real poles are real and independent, and K, M
+// are real, so their COCG vectors travel as the two components of one
+// 16-byte value through the complex layout, tensor maps and tiles, with
+// every operation component-wise (no cross terms: fewer FP64 operations than
+// a complex shift at the same bytes).
+struct dpair {
+  double x, y;
+};
+__device__ __forceinline__ dpair make_dpair(double x, double y) {
+  dpair r;
+  r.x = x;
+  r.y = y;
+  return r;
+}
+__device__ __forceinline__ dpair cadd(dpair a, dpair b) { return make_dpair(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ dpair csub(dpair a, dpair b) { return make_dpair(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ dpair cscale(double s, dpair a) { return make_dpair(s * a.x, s * a.y); }
+__device__ __forceinline__ dpair cmul(dpair a, dpair b) { return make_dpair(a.x * b.x, a.y * b.y); }
+__device__ __forceinline__ dpair cfma(dpair b, dpair c, dpair a) {
+  return make_dpair(fma(b.x, c.x, a.x), fma(b.y, c.y, a.y));
+}
+__device__ __forceinline__ dpair cdiv(dpair a, dpair b) { return make_dpair(a.x / b.x, a.y / b.y); }
+__device__ __forceinline__ dpair csq(dpair a) { return make_dpair(a.x * a.x, a.y * a.y); }
+__device__ __forceinline__ dpair crcp(dpair b, dpair& n) {
+  double nx, ny;
+  const double rx = crcp(b.x, nx), ry = crcp(b.y, ny);
+  n = make_dpair(nx, ny);
+  return make_dpair(rx, ry);
+}
+
 // acc + s * a for a real scalar s (component-wise fma)
 __device__ __forceinline__ double2 sfma(double s, double2 a, double2 acc) {
   return make_double2(fma(s, a.x, acc.x), fma(s, a.y, acc.y));
 }
 __device__ __forceinline__ double sfma(double s, double a, double acc) { return fma(s, a, acc); }
+__device__ __forceinline__ dpair sfma(double s, dpair a, dpair acc) {
+  return make_dpair(fma(s, a.x, acc.x), fma(s, a.y, acc.y));
+}
 
 template <typename V>
 struct VT;
 template <>
 struct VT<double2> {
   static constexpr bool kReal = false;
+  static constexpr bool kPair = false;
+  typedef double R;
+  __device__ __forceinline__ static double2 diag(double kd, double m, double2 sh) {
+    return make_double2(kd + m * sh.x, m * sh.y);
+  }
+  __device__ __forceinline__ static R rzero() { return 0.0; }
+  __device__ __forceinline__ static R rone() { return 1.0; }
+  __device__ __forceinline__ static R abs2(double2 v) { return fma(v.x, v.x, v.y * v.y); }
+  __device__ __forceinline__ static R rfma(R a, R b, R c) { return fma(a, b, c); }
+  __device__ __forceinline__ static bool small_beta(double2 beta, double2, double2, double thr) {
+    return fma(beta.x, beta.x, beta.y * beta.y) < thr;
+  }
+  __device__ __forceinline__ static double2 div0(double2 a, double2 b) { return cdiv(a, b); }
+  __device__ __forceinline__ static double r0(R r) { return r; }
+  __device__ __forceinline__ static double r1(R) { return 0.0; }
   __device__ __forceinline__ static double2 zero() { return make_double2(0.0, 0.0); }
   __device__ __forceinline__ static double2 from(double2 v) { return v; }     // scalar state -> V
   __device__ __forceinline__ static double2 cplx(double2 v) { return v; }     // V -> complex
@@ -111,8 +160,48 @@ struct VT<double2> {
   __device__ __forceinline__ static double im(double2 v) { return v.y; }
 };
 template <>
+struct VT<dpair> {
+  static constexpr bool kReal = false;   // complex layout (16-byte slots)
+  static constexpr bool kPair = true;
+  typedef dpair R;                       // squared magnitudes, one per component
+  __device__ __forceinline__ static dpair zero() { return make_dpair(0.0, 0.0); }
+  __device__ __forceinline__ static dpair from(double2 v) { return make_dpair(v.x, v.y); }   // packed (A, B)
+  __device__ __forceinline__ static double2 cplx(dpair v) { return make_double2(v.x, v.y); }  // packed (A, B)
+  __device__ __forceinline__ static dpair diag(double kd, double m, dpair sh) {
+    return make_dpair(fma(m, sh.x, kd), fma(m, sh.y, kd));
+  }
+  __device__ __forceinline__ static R rzero() { return make_dpair(0.0, 0.0); }
+  __device__ __forceinline__ static R rone() { return make_dpair(1.0, 1.0); }
+  __device__ __forceinline__ static R abs2(dpair v) { return make_dpair(v.x * v.x, v.y * v.y); }
+  __device__ __forceinline__ static R rfma(R a, R b, R c) { return make_dpair(fma(a.x, b.x, c.x), fma(a.y, b.y, c.y)); }
+  // R11: p_{i-1} must be re-read when a component that still moves x has a small beta;
+  // a frozen member (alpha = alpha_prev = 0, beta = 0) adds nothing to x and does not count
+  __device__ __forceinline__ static bool small_beta(dpair beta, dpair alpha, dpair alpha_prev, double thr) {
+    const bool mx = alpha.x != 0.0 || alpha_prev.x != 0.0, my = alpha.y != 0.0 || alpha_prev.y != 0.0;
+    return (mx && beta.x * beta.x < thr) || (my && beta.y * beta.y < thr);
+  }
+  __device__ __forceinline__ static dpair div0(dpair a, dpair b) {   // a / b, 0 where b = 0
+    return make_dpair(b.x != 0.0 ? a.x / b.x : 0.0, b.y != 0.0 ? a.y / b.y : 0.0);
+  }
+  __device__ __forceinline__ static double r0(R r) { return r.x; }
+  __device__ __forceinline__ static double r1(R r) { return r.y; }
+};
+template <>
 struct VT<double> {
   static constexpr bool kReal = true;
+  static constexpr bool kPair = false;
+  typedef double R;
+  __device__ __forceinline__ static double diag(double kd, double m, double sh) { return fma(m, sh, kd); }
+  __device__ __forceinline__ static R rzero() { return 0.0; }
+  __device__ __forceinline__ static R rone() { return 1.0; }
+  __device__ __forceinline__ static R abs2(double v) { return v * v; }
+  __device__ __forceinline__ static R rfma(R a, R b, R c) { return fma(a, b, c); }
+  __device__ __forceinline__ static bool small_beta(double beta, double, double, double thr) {
+    return beta * beta < thr;
+  }
+  __device__ __forceinline__ static double div0(double a, double b) { return a / b; }
+  __device__ __forceinline__ static double r0(R r) { return r; }
+  __device__ __forceinline__ static double r1(R) { return 0.0; }
   __device__ __forceinline__ static double zero() { return 0.0; }
   __device__ __forceinline__ static double from(double2 v) { return v.x; }
   __device__ __forceinline__ static double2 cplx(double v) { return make_double2(v, 0.0); }

@@ -331,7 +331,8 @@ __global__ void __launch_bounds__(256) k_dsynth_mnorm(long long nslots, const do
 // snapshot taken when shift s first reached 10x its tolerance and the end of
 // the first solve, d_s = x_s - snap_s (complex layout), and its M-weighted
 // moments sum m (Re d)^2, sum m (Im d)^2, sum m Re d Im d -> part[(s*3+t)*gridDim.x + x].
-// mode[s]: 0 no snapshot (d_s = 0), 1 complex snapshot, 2 real-layout snapshot.
+// mode[s]: 0 no snapshot (d_s = 0), 1 complex snapshot, 2 real-layout snapshot,
+// 3 / 4 snapshot of a pair's packed block: this shift is component x / y (R16).
 struct SnapArgs {
   Grid g;
   const double* mass;
@@ -359,6 +360,8 @@ __global__ void __launch_bounds__(256) k_snap_delta(const __grid_constant__ Snap
       double2 sv;
       if (mode == 1) {
         sv = sc[e];
+      } else if (mode >= 3) {
+        sv = make_double2(mode == 3 ? sc[e].x : sc[e].y, 0.0);
       } else {
         const long long c = e / g.Nn, node = e - c * g.Nn;
         sv = make_double2(sr[c * g.NnP + (node / nx1) * g.px + node % nx1 + 1], 0.0);

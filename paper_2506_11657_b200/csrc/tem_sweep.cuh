@@ -87,7 +87,15 @@ struct ShiftState {
   int iters;
   int status;       // 0 running, 1 converged, 2 breakdown
   int real;         // 1: real shift and real right-hand side -> real arithmetic (split scheme)
+  int pair;         // partner shift + 1 of a pair of real shifts sharing one slot (R16), 0: none
+  int lead;         // 1: component x of the pair (its block holds the packed vectors), 0: component y
 };
+
+// Control::list entry of a slot: the shift (leader of a pair) in bits 0..7,
+// partner + 1 in bits 8..15.
+__host__ __device__ __forceinline__ int slot_code(int s, int partner) { return s | ((partner + 1) << 8); }
+__host__ __device__ __forceinline__ int slot_shift(int code) { return code & 255; }
+__host__ __device__ __forceinline__ int slot_partner(int code) { return (code >> 8) - 1; }
 
 struct Control {
   int n_active;           // number of active shifts
@@ -120,8 +128,9 @@ struct SweepArgs {
 
 // Split solver (MODE 3/4 pass 1, k_delta pass 2) per-CTA partials:
 // [0..6] pass 1: gamma, eps, mu (re, im), ||r||^2; [7, 8] pass 2: z^T K z;
-// [9, 10] pass 1: s sum_e m_e z_e^2 (the mass part of delta, pointwise)
-constexpr int kSplitPart = 11;
+// [9, 10] pass 1: s sum_e m_e z_e^2 (the mass part of delta, pointwise);
+// [11] pass 1: ||r||^2 of shift B of a pair of real shifts ([6]: shift A)
+constexpr int kSplitPart = 12;
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -183,6 +192,16 @@ __device__ __forceinline__ double ld_mass(const double* p, uint64_t pol) {
 // (measured: split pass 1 odd -4%).
 __device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(double* p, double v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(dpair* p, dpair v) {
+  __stcs(reinterpret_cast<double2*>(p), make_double2(v.x, v.y));
+}
+// own-value loads through L2 (ld.global.cg)
+__device__ __forceinline__ double2 ld_cgv(const double2* p) { return __ldcg(p); }
+__device__ __forceinline__ double ld_cgv(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ dpair ld_cgv(const dpair* p) {
+  const double2 v = __ldcg(reinterpret_cast<const double2*>(p));
+  return make_dpair(v.x, v.y);
+}
 
 // q mod n for q >= -8n (ring slots of plane sets; sets start at kb - 2 >= -2)
 __device__ __forceinline__ int pmod(int q, int n) { return (int)((unsigned)(q + 8 * n) % (unsigned)n); }
@@ -397,17 +416,86 @@ __device__ __forceinline__ ShiftState ld_state(const ShiftState* p) {
 }
 __device__ __forceinline__ int ld_cg(const int* p) { return __ldcg(p); }
 
+// One shift's scalar update from its sums (real shifts and the members of a
+// pair pass zero imaginary parts): returns with sq updated.
+template <bool PRIME>
+__device__ __forceinline__ void split_update(ShiftState& sq, double2 gam, double2 eps, double2 mu, double2 dk,
+                                             double2 dm, double rr) {
+  if (PRIME) {
+    const double2 del0 = cadd(dk, sq.dm0);
+    if (del0.x == 0.0 && del0.y == 0.0) {
+      sq.active = 0;
+      sq.status = 2;
+    } else {
+      sq.alpha = cdiv(sq.rho, del0);
+      sq.alpha_prev = czero();
+      sq.beta = czero();
+    }
+    return;
+  }
+  const double2 del = cadd(dk, dm);   // z^T K z + s z^T M z
+  sq.iters += 1;
+  sq.relres = sqrt(rr) / sq.fnorm;
+  if (sq.relres <= sq.tol) {
+    sq.active = 0;
+    sq.status = 1;
+  } else if ((gam.x == 0.0 && gam.y == 0.0) || (sq.rho.x == 0.0 && sq.rho.y == 0.0)) {
+    sq.active = 0;
+    sq.status = 2;
+  } else {
+    const double2 beta = cdiv(gam, sq.rho);
+    const double2 den = cadd(del, cmul(beta, cadd(cscale(2.0, eps), cmul(beta, mu))));
+    if (den.x == 0.0 && den.y == 0.0) {
+      sq.active = 0;
+      sq.status = 2;
+    } else {
+      sq.beta = beta;
+      sq.alpha_prev = sq.alpha;
+      sq.alpha = cdiv(gam, den);
+      sq.rho = gam;
+    }
+  }
+}
+
+// A member of a pair that has stopped while its partner runs on is frozen:
+// alpha = beta = 0 (p = z, z unchanged), and its last step length moves to
+// alpha_prev once, so the next odd pass (or k_xfix) still adds alpha_i p_i to
+// x exactly once (R11, R16).
+__device__ __forceinline__ void pair_freeze(ShiftState& sq) {
+  sq.alpha_prev = sq.alpha;
+  sq.alpha = czero();
+  sq.beta = czero();
+}
+
+// The active slots: a single shift while it is active, a pair while either
+// member is (the leader carries the slot).  Called by the whole first warp
+// (S <= 32: one shift per lane, one L2 round trip instead of a serial scan --
+// the scan was ~4 us per iteration, a tenth of an iteration of `block`).
+__device__ __forceinline__ void rebuild_list(const SweepArgs& A) {
+  const int lane = threadIdx.x & 31;
+  const bool has = lane < A.S;
+  const int partner = has ? ld_cg(&A.st[lane].pair) - 1 : -1;
+  const int lead = has ? ld_cg(&A.st[lane].lead) : 0;
+  const int act = has ? ld_cg(&A.st[lane].active) : 0;
+  const int pact = __shfl_sync(0xffffffffu, act, partner >= 0 ? partner : 0);
+  const bool slot = has && (partner < 0 ? act != 0 : (lead && (act || pact)));
+  const unsigned mask = __ballot_sync(0xffffffffu, slot);
+  if (slot) A.ctl->list[__popc(mask & ((1u << lane) - 1u))] = slot_code(lane, partner);
+  if (lane == 0) A.ctl->n_active = __popc(mask);
+}
+
 template <bool PRIME, int TYV>
 __device__ void finalize_split(const SweepArgs& A, int ns, int per) {
   // ns: shift slots of the pass; per: work units (partials) per slot
   constexpr int NT = Tile<TYV>::NT;
-  const int S = A.S;
   const int n_list = ld_cg(&A.ctl->n_active);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int a = warp; a < ns && a < n_list; a += NT / 32) {
-    const int sidx = ld_cg(&A.ctl->list[a]);
-    ShiftState sq = ld_state(&A.st[sidx]);
-    if (!sq.active) continue;
+    const int code = ld_cg(&A.ctl->list[a]);
+    const int sidx = slot_shift(code), pidx = slot_partner(code);
+    const bool act_a = ld_cg(&A.st[sidx].active) != 0;
+    const bool act_b = pidx >= 0 && ld_cg(&A.st[pidx].active) != 0;
+    if (!act_a && !act_b) continue;
     double v[kSplitPart];
 #pragma unroll
     for (int t = 0; t < kSplitPart; ++t) {
@@ -417,53 +505,35 @@ __device__ void finalize_split(const SweepArgs& A, int ns, int per) {
       v[t] = warp_sum(acc);
     }
     if (lane != 0) continue;
-    const double2 gam = make_double2(v[0], v[1]), eps = make_double2(v[2], v[3]);
-    const double2 mu = make_double2(v[4], v[5]);
-    const double2 del = make_double2(v[7] + v[9], v[8] + v[10]);   // z^T K z + s z^T M z
-    if (PRIME) {
-      const double2 del0 = make_double2(v[7] + sq.dm0.x, v[8] + sq.dm0.y);
-      if (del0.x == 0.0 && del0.y == 0.0) {
-        sq.active = 0;
-        sq.status = 2;
-      } else {
-        sq.alpha = cdiv(sq.rho, del0);
-        sq.alpha_prev = czero();
-        sq.beta = czero();
-      }
+    if (pidx < 0) {
+      ShiftState sq = ld_state(&A.st[sidx]);
+      split_update<PRIME>(sq, make_double2(v[0], v[1]), make_double2(v[2], v[3]), make_double2(v[4], v[5]),
+                          make_double2(v[7], v[8]), make_double2(v[9], v[10]), v[6]);
       A.st[sidx] = sq;
       continue;
     }
-    sq.iters += 1;
-    sq.relres = sqrt(v[6]) / sq.fnorm;
-    if (sq.relres <= sq.tol) {
-      sq.active = 0;
-      sq.status = 1;
-    } else if ((gam.x == 0.0 && gam.y == 0.0) || (sq.rho.x == 0.0 && sq.rho.y == 0.0)) {
-      sq.active = 0;
-      sq.status = 2;
-    } else {
-      const double2 beta = cdiv(gam, sq.rho);
-      const double2 den = cadd(del, cmul(beta, cadd(cscale(2.0, eps), cmul(beta, mu))));
-      if (den.x == 0.0 && den.y == 0.0) {
-        sq.active = 0;
-        sq.status = 2;
-      } else {
-        sq.beta = beta;
-        sq.alpha_prev = sq.alpha;
-        sq.alpha = cdiv(gam, den);
-        sq.rho = gam;
+    // a pair: component x is shift sidx, component y its partner, both real
+    // (one member at a time: one ShiftState live)
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      const int q = h ? pidx : sidx;
+      ShiftState sq = ld_state(&A.st[q]);
+      if (h ? act_b : act_a) {
+        split_update<PRIME>(sq, make_double2(v[0 + h], 0.0), make_double2(v[2 + h], 0.0),
+                            make_double2(v[4 + h], 0.0), make_double2(v[7 + h], 0.0),
+                            make_double2(v[9 + h], 0.0), h ? v[11] : v[6]);
+        if (!sq.active) pair_freeze(sq);
+      } else if (!PRIME) {
+        pair_freeze(sq);
       }
+      A.st[q] = sq;
     }
-    A.st[sidx] = sq;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
     __threadfence();
-    int na = 0;
-    for (int q = 0; q < S; ++q)
-      if (ld_cg(&A.st[q].active)) A.ctl->list[na++] = q;
-    A.ctl->n_active = na;
-    A.ctl->ticket[PRIME ? 6 : 5] = 0;
+    rebuild_list(A);
+    if (threadIdx.x == 0) A.ctl->ticket[PRIME ? 6 : 5] = 0;
   }
 }
 
@@ -604,8 +674,9 @@ __device__ __forceinline__ constexpr int vofs() {
 // The split modes run a real shift (ShiftState::real) in real arithmetic:
 // the same body over V = double, half-size tiles in the same ring slots.
 struct Partials {
-  double2 c, e, m, q;
-  double r;
+  double2 c, e, m;   // gamma (MODE 1: p^T A p), eps, mu; a pair of real shifts: (A, B) in (x, y)
+  double2 dm;        // split: s z^T M z (the mass part of delta)
+  double r, r2;      // ||r||^2 (r2: shift B of a pair)
 };
 
 // The vectors one sweep reads and writes (per iteration parity).
@@ -644,16 +715,17 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
   const V sh = VT<V>::from(sh2), alpha = VT<V>::from(alpha2), beta = VT<V>::from(beta2);
   const V alpha_prev = VT<V>::from(alpha_prev2);
   V acc_c = VT<V>::zero(), acc_e = VT<V>::zero(), acc_m = VT<V>::zero(), acc_q = VT<V>::zero();
-  double acc_r = 0.0;
+  typename VT<V>::R acc_r = VT<V>::rzero();
   // MODE 4: x_{i+1} = x_{i-1} + (alpha_i + a/beta_i) p_i - (a/beta_i) z_i, a = alpha_{i-1}
   // (exact rewrite of alpha_{i-1} p_{i-1} + alpha_i p_i).  Its rounding error,
   // relative to the x increment, grows like |z_i| / |beta_i p_{i-1}|; when
   // |beta_i| < 1/32 (about 2% of iterations) p_{i-1} is re-read instead (x_direct).
-  const bool x_direct = MODE == 4 && (A.force_xdirect || cabs2(beta) < 1.0 / 1024.0);
+  const bool x_direct =
+      MODE == 4 && (A.force_xdirect || VT<V>::small_beta(beta, alpha, alpha_prev, 1.0 / 1024.0));
   // x_{i+1} = x_{i-1} + xc_p p_i + xc_z (z_i, or p_{i-1} when x_direct)
   V xc_p = alpha, xc_z = alpha_prev;
   if (MODE == 4 && !x_direct) {
-    xc_z = cdiv(alpha_prev, beta);
+    xc_z = VT<V>::div0(alpha_prev, beta);
     xc_p = cadd(alpha, xc_z);
     xc_z = cscale(-1.0, xc_z);
   }
@@ -765,8 +837,8 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
         xN[c] = xv[TEM_EI(slot)];
         zN[c] = zv[TEM_EI(slot)];
       }
-      if (MODE == 4) xN[c] = __ldcg(xv + TEM_EI(slot));
-      if (kUpd && !kZOwn) zN[c] = __ldcg(zin + TEM_EI(slot));
+      if (MODE == 4) xN[c] = ld_cgv(xv + TEM_EI(slot));
+      if (kUpd && !kZOwn) zN[c] = ld_cgv(zin + TEM_EI(slot));
     }
   };
   load_centre(kb);
@@ -803,20 +875,20 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
       const auto e = TEM_EI(ek + c * cst);
       const V q = cfma(sh, cscale(mN[c], E.p[c]), E.q[c]);   // (K + s M) v
       if (kUpd) {
-        const V D = VT<V>::make(E.kd[c] + mN[c] * sh2.x, mN[c] * sh2.y);
-        double nD;                                                      // |D|^2
+        const V D = VT<V>::diag(E.kd[c], mN[c], sh);
+        typename VT<V>::R nD;                                           // |D|^2
         const V zn = csub(zN[c], cmul(alpha, cmul(q, crcp(D, nD))));   // z_i - alpha D^-1 A p_i
         st_stream(out + e, E.p[c]);                                     // p_i
         st_stream(zv + e, zn);                                          // z_{i+1}
         if (MODE == 4) {   // x_{i+1} = x_{i-1} + alpha_{i-1} p_{i-1} + alpha_i p_i
           if (x_direct)
-            st_stream(xv + e, cfma(xc_p, E.p[c], cfma(xc_z, __ldcg(pold + e), xN[c])));
+            st_stream(xv + e, cfma(xc_p, E.p[c], cfma(xc_z, ld_cgv(pold + e), xN[c])));
           else   // p_{i-1} = (p_i - z_i) / beta_i: no re-read of p_{i-1}
             st_stream(xv + e, cfma(xc_z, zN[c], cfma(xc_p, E.p[c], xN[c])));
         }
         const V zq = csq(zn);                                           // z_{i+1}^2
         acc_c = sfma(E.kd[c], zq, acc_c);            // gamma_{i+1} = (D z)^T z = sum kd z^2 + s z^T M z
-        acc_r = fma(nD, cabs2(zn), acc_r);           // ||D z||^2
+        acc_r = VT<V>::rfma(nD, VT<V>::abs2(zn), acc_r);   // ||D z||^2
         acc_q = sfma(mN[c], zq, acc_q);              // z^T M z
         acc_e = cfma(zn, q, acc_e);                  // z_{i+1}^T A p_i
         acc_m = cfma(E.p[c], q, acc_m);              // p_i^T A p_i
@@ -826,13 +898,13 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
         st_stream(out + e, E.p[c]);      // p_new
         acc_c = cfma(E.p[c], q, acc_c);  // p^T A p
       } else {
-        const V D = VT<V>::make(E.kd[c] + mN[c] * sh2.x, mN[c] * sh2.y);
+        const V D = VT<V>::diag(E.kd[c], mN[c], sh);
         st_stream(xv + e, cfma(alpha, E.p[c], xN[c]));
         const V zn = csub(zN[c], cmul(alpha, cdiv(q, D)));   // z - alpha D^-1 q
         st_stream(zv + e, zn);
         const V rn = cmul(D, zn);                           // r = D z
         acc_c = cfma(rn, zn, acc_c);
-        acc_r += cabs2(rn);
+        acc_r = VT<V>::rfma(VT<V>::abs2(rn), VT<V>::rone(), acc_r);
       }
     }
     // centre operands of step k+1: issued now, consumed after step k+1's stencil
@@ -846,11 +918,13 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
     }
   }
   // gamma = sum (kd + s m) z^2: the mass part s z^T M z is acc_q (MODE 3/4)
-  P.c = kUpd ? cadd(VT<V>::cplx(acc_c), cmul(sh2, VT<V>::cplx(acc_q))) : VT<V>::cplx(acc_c);
+  const V dm = cmul(sh, acc_q);   // s z^T M z
+  P.c = VT<V>::cplx(kUpd ? cadd(acc_c, dm) : acc_c);
   P.e = VT<V>::cplx(acc_e);
   P.m = VT<V>::cplx(acc_m);
-  P.q = VT<V>::cplx(acc_q);
-  P.r = acc_r;
+  P.dm = VT<V>::cplx(dm);
+  P.r = VT<V>::r0(acc_r);
+  P.r2 = VT<V>::r1(acc_r);
 #undef TEM_EI
 }
 
@@ -860,8 +934,7 @@ template <int NT>
 __device__ __forceinline__ void write_split_partials(const SweepArgs& A, const Partials& P, double2 sh, int pidx) {
   __shared__ double red9[kSplitPart * NT / 32];
   const int tid = threadIdx.x;
-  const double2 dm = cmul(sh, P.q);   // s z^T M z
-  double v[kSplitPart] = {P.c.x, P.c.y, P.e.x, P.e.y, P.m.x, P.m.y, P.r, 0.0, 0.0, dm.x, dm.y};
+  double v[kSplitPart] = {P.c.x, P.c.y, P.e.x, P.e.y, P.m.x, P.m.y, P.r, 0.0, 0.0, P.dm.x, P.dm.y, P.r2};
 #pragma unroll
   for (int t = 0; t < kSplitPart; ++t)
     if (t < 7 || t > 8)
@@ -900,15 +973,18 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
   const int tid = threadIdx.x;
 
   double2 sh = czero(), alpha = czero(), beta = czero(), alpha_prev = czero();
-  bool live, real = false;
+  bool live, real = false, pair = false;
   int s = a;
   if (MODE == 0) {
     sh = A.shifts[s];
     live = true;
   } else {
-    live = a < A.ctl->n_active;
+    // n_active and list[a] share a cache line: both loads go out together (one L2
+    // round trip instead of two dependent ones ahead of every CTA's first TMA)
+    const int n_act = A.ctl->n_active, code = A.ctl->list[a & 31];
+    live = a < n_act;
     if (live) {
-      s = A.ctl->list[a];
+      s = slot_shift(code);
       const ShiftState& st = A.st[s];
       sh = st.s;
       alpha = st.alpha;
@@ -916,6 +992,15 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
       alpha_prev = st.alpha_prev;
       live = st.active != 0;
       real = kUpd && st.real;
+      if (kUpd && slot_partner(code) >= 0) {   // two real shifts: scalars packed (A, B) component-wise
+        const ShiftState& sb = A.st[slot_partner(code)];
+        pair = true;
+        sh.y = sb.s.x;
+        alpha.y = sb.alpha.x;
+        beta.y = sb.beta.x;
+        alpha_prev.y = sb.alpha_prev.x;
+        live = live || sb.active != 0;
+      }
     }
   }
   Partials P{};
@@ -923,7 +1008,10 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
   const Bufs B = bufs_of(A);
   if (live) {
     if constexpr (kUpd) {
-      if (real)
+      if (pair)
+        sweep_body<MODE, TYV, dpair>(A, &tmv, &tmz, s, tx0, ty0, kb, ke, sh, alpha, beta, alpha_prev, ring,
+                                     bar, phase, true, zih, zhd, P, B);
+      else if (real)
         sweep_body<MODE, TYV, double>(A, &tmvr, &tmzr, s, tx0, ty0, kb, ke, sh, alpha, beta, alpha_prev,
                                       ring, bar, phase, true, zih, zhd, P, B);
       else
@@ -1028,18 +1116,25 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, 768 / Tile<TYV>::NT)
   int pidx;
   block_coords<TYV>(A, a, tx0, ty0, kb, ke, pidx);
   const int tid = threadIdx.x;
-  bool live = a < A.ctl->n_active;
+  const int n_act = A.ctl->n_active, code = A.ctl->list[a & 31];   // one cache line, one round trip
+  bool live = a < n_act;
   int s = 0;
-  bool real = false;
+  bool real = false, pair = false;
   if (live) {
-    s = A.ctl->list[a];
+    s = slot_shift(code);
     live = A.st[s].active != 0;
     real = A.st[s].real != 0;
+    if (slot_partner(code) >= 0) {
+      pair = true;
+      live = live || A.st[slot_partner(code)].active != 0;
+    }
   }
   double2 acc = czero();
   uint32_t phase = 0;
   if (live) {
-    if (real)
+    if (pair)
+      acc = delta_body<TYV, dpair>(A, &tmv, s, tx0, ty0, kb, ke, ring, bar, phase, true, zih, zhd);
+    else if (real)
       acc = delta_body<TYV, double>(A, &tmvr, s, tx0, ty0, kb, ke, ring, bar, phase, true, zih, zhd);
     else
       acc = delta_body<TYV, double2>(A, &tmv, s, tx0, ty0, kb, ke, ring, bar, phase, true, zih, zhd);

@@ -92,6 +92,42 @@ def test_real_shifts_in_real_arithmetic(monkeypatch):
         assert abs(int(iters[i]) - int(iters2[i])) <= 0.25 * iters2[i] + 20
 
 
+def test_paired_real_shifts_match_single(monkeypatch):
+    """Reading R16: real shifts run two to a slot (component-wise arithmetic in
+    the complex layout).  Same arithmetic per component as the single real
+    path, so x agrees to rounding (the x bookkeeping of R11 may take the
+    re-read path for both members when one beta is small), iteration counts
+    agree, imaginary parts are exactly 0, and a member that stops early is
+    frozen while its partner runs on (different per-shift tolerances)."""
+    wl = make_workload("block")
+    table = RationalTable.load("block")
+    real = np.nonzero(table.shifts.imag == 0)[0]
+    assert len(real) == 4
+    fw, asm, slots, sigma, f = _setup(wl, table)
+    mass = fw.edge_mass(sigma)
+    shifts = table.shifts[real[:3]]            # one pair + a single real shift
+    x, iters, relres = fw.cocg(mass, f, shifts, tol=1e-11, maxit=60000)
+    monkeypatch.setenv("TEM_NO_PAIR", "1")
+    x1, iters1, relres1 = fw.cocg(mass, f, shifts, tol=1e-11, maxit=60000)
+    monkeypatch.delenv("TEM_NO_PAIR")
+    xg, x1g = x.cpu().numpy(), x1.cpu().numpy()
+    assert np.all(xg.imag == 0.0)
+    for i in range(3):
+        d = np.linalg.norm(xg[i] - x1g[i]) / np.linalg.norm(x1g[i])
+        assert d < 1e-9, (i, d)
+        assert abs(int(iters[i]) - int(iters1[i])) <= 0.05 * iters1[i] + 5, (iters, iters1)
+        assert ofw.relative_residual(asm, shifts[i], xg[i][slots]) <= 1.05e-11, i
+    # members with very different stopping times: per-shift tolerances through the rhs solve
+    rhs = f.to(torch.complex128).unsqueeze(0).repeat(4, 1).contiguous()
+    tols = np.array([1e-4, 1e-11, 1e-11, 1e-3])
+    xr, itr, rr = fw.cocg_rhs(mass, rhs, table.shifts[real], tols, maxit=60000)
+    xrg = xr.cpu().numpy()
+    assert np.all(xrg.imag == 0.0)
+    for i, s in enumerate(table.shifts[real]):
+        assert ofw.relative_residual(asm, s, xrg[i][slots]) <= 1.05 * tols[i], (i, itr)
+    assert itr[0] < itr[1] and itr[3] < itr[2]
+
+
 def _pow2_workload():
     """Uniform 32 m cells and power-of-two conductivities: every face weight
     and edge mass is one correctly rounded quotient times a power of two on
