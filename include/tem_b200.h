@@ -112,7 +112,12 @@ size_t tem_cocg_workspace_bytes(const tem_ctx* ctx, int S);
  *   iters, relres (HOST, may be NULL): per-shift iteration count and final
  *           recursive relative residual.
  * Returns after the solve has finished (synchronises `stream`).
- * TEM_ENOCONV if some shift did not reach tol (x still holds its iterate). */
+ * TEM_ENOCONV if some shift did not reach tol (x still holds its iterate).
+ * TEM_EINVAL if S * 6 * nodes >= 2^32 (the sweeps index a shift block with
+ * unsigned 32-bit element indices; HBM capacity is the tighter limit).
+ * Real shifts (imag == 0; footnote to eq:rmj) run in real
+ * arithmetic in the split scheme, two to a slot where there are two
+ * (readings R14, R16); their x has imaginary part exactly 0. */
 int tem_cocg_solve(tem_ctx* ctx, const double* mass, const double* f, int S,
                    const double* shifts, double tol, int maxit, double* x,
                    void* work, size_t work_bytes, int* iters, double* relres,
