@@ -545,11 +545,14 @@ static void sweep_geometry(const tem_ctx* c, int S, int nslot, tem::SweepArgs& A
   const int base = A.ntx * A.nty * nslot;
   // z-chunk count.  W = CTAs / resident CTAs.
   // Bandwidth regime (some candidate reaches >= 4 waves with >= 8 planes per
-  // chunk): keep >= 4 waves (a few slow shifts must still fill the machine)
-  // and among those maximise (wave quantisation W / ceil(W): a partial last
-  // wave idles SMs) x (march efficiency kch / (kch + 3): a CTA fills its plane
-  // pipeline, ~3 steps, before it computes).  Large config, 14 shifts: 1344
-  // columns = 9.08 waves of 148 -> 2 chunks of 64 planes, 18.2 waves.
+  // chunk): keep ~2 waves or more and among those maximise (wave quantisation
+  // W / ceil(W): a partial last wave idles SMs) x (march efficiency
+  // kch / (kch + 3): a CTA fills its plane pipeline, ~3 steps, before it
+  // computes).  Large config, 12 slots: 1152 columns = 7.8 waves of 148 -> 2
+  // chunks of 64 planes, 15.6 waves; one slot left: 3 chunks of 43 planes,
+  // 1.95 waves (measured 0.294 ms per iteration against 0.362 ms with the 9
+  // chunks a 4-wave floor asked for; CTA durations are uniform now that real
+  // shifts run in pairs, R16; `scripts/nzc_tail.sh`).
   // Latency regime (small grids, few active shifts: the whole sweep is less
   // than 4 waves): minimise the critical path, ceil(W) waves of (kch + 3)
   // plane steps each, down to one plane per chunk -- e.g. `block` with one
@@ -564,6 +567,8 @@ static void sweep_geometry(const tem_ctx* c, int S, int nslot, tem::SweepArgs& A
     const int nz_eff = (nz + kch - 1) / kch;
     bandwidth |= (double)base * nz_eff / slots_sm >= 4.0;
   }
+  double min_waves = 1.9;
+  if (const char* env = getenv("TEM_MIN_WAVES")) min_waves = atof(env);   // experiments
   double best = bandwidth ? -1.0 : 1e300;
   for (int cand = nzc_min; cand <= (bandwidth ? 32 : std::min(nz, 64)); ++cand) {
     const int kch = (nz + cand - 1) / cand;
@@ -572,7 +577,7 @@ static void sweep_geometry(const tem_ctx* c, int S, int nslot, tem::SweepArgs& A
     const double W = (double)base * nz_eff / slots_sm;
     if (bandwidth) {
       if (cand != nzc_min && nz / cand < 8) break;
-      if (W < 4.0) continue;
+      if (W < min_waves) continue;
       const double score = W / std::ceil(W) * (double)kch / (kch + 3.0);
       if (score > best + 1e-9) {
         best = score;
