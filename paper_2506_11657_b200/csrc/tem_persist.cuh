@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, 1)
                                         st.alpha_prev, ring, bar_s, ph_s, false, zih, zhd, P, B);
         }
       }
-      write_split_partials<NT>(A, P, st.s, pidx);
+      write_split_partials<NT>(A, P, pidx);
     }
     grid_sync(PA.gbar);
     // ---- pass 2: delta = z_{i+1}^T K z_{i+1}

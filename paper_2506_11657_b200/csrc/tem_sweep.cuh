@@ -931,7 +931,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs& A, const CUtensorMap
 // Split pass 1: the CTA's partial sums (gamma, eps, mu, ||r||^2, s z^T M z)
 // -> A.part[t][pidx] (fixed-order block reduction, deterministic).
 template <int NT>
-__device__ __forceinline__ void write_split_partials(const SweepArgs& A, const Partials& P, double2 sh, int pidx) {
+__device__ __forceinline__ void write_split_partials(const SweepArgs& A, const Partials& P, int pidx) {
   __shared__ double red9[kSplitPart * NT / 32];
   const int tid = threadIdx.x;
   double v[kSplitPart] = {P.c.x, P.c.y, P.e.x, P.e.y, P.m.x, P.m.y, P.r, 0.0, 0.0, P.dm.x, P.dm.y, P.r2};
@@ -1024,7 +1024,7 @@ __global__ void __launch_bounds__(Tile<TYV>::NT, Tile<TYV>::kMinBlocks)
   }
   if (MODE == 0) return;
   if (kUpd) {
-    write_split_partials<NT>(A, P, sh, pidx);
+    write_split_partials<NT>(A, P, pidx);
     return;
   }
   double2 acc_c = P.c;
