@@ -38,7 +38,9 @@ for ln in res.stderr.splitlines():
         continue
     if "persistent" in ln:
         continue
-    kv = dict(t.split("=") for t in ln.split()[2:])
+    kv = dict(t.split("=", 1) for t in ln.split()[2:] if "=" in t)
+    if "slots" not in kv or "chunk_ms" not in kv:   # other trace lines (refinement rounds)
+        continue
     key = (int(kv["slots"]), int(kv["nzc"]))
     a = agg.setdefault(key, [0, 0.0])
     a[0] += 1
@@ -46,4 +48,4 @@ for ln in res.stderr.splitlines():
 tot = sum(v[1] for v in agg.values())
 for (slots, nzc), (n, ms) in sorted(agg.items(), reverse=True):
     print(f"slots {slots:2d} nzc {nzc:2d}: {n:4d} graphs  {ms:9.1f} ms  ({100*ms/tot:5.1f}%)  "
-          f"{ms/n/16:.3f} ms/iter  {ms/n/16/slots:.3f} ms/shift-iter")
+          f"{ms/n/16:.3f} ms/iter  {ms/n/16/slots:.3f} ms/slot-iter")
